@@ -1,0 +1,136 @@
+/*
+ * lego_b200.h -- C ABI of the B200 execution backend for the LEGO layout
+ * language (arXiv 2505.08091).
+ *
+ * The reference package (/root/reference/pkg/src/lego) is pure Python and
+ * has no FFI; its hot path is the per-element scalar call
+ *     GroupBy.apply(idx)  (layout.py:313-318)   logical index -> position
+ *     GroupBy.inv(flat)   (layout.py:320-328)   position -> logical index
+ * (ExpandBy.apply/inv, layout.py:383-400, for partial tiles) looped over a
+ * whole index space by user code, template.instantiate or the CLI
+ * (cli.py:166-198).  Each entry point below replaces such a loop with one
+ * stream-ordered launch; INTEGRATION.md shows the ctypes binding the
+ * reference would add.
+ *
+ * Conventions: every function returns lego_status (0 = OK) and never throws;
+ * lego_last_error() holds a thread-local message for the last failure.  All
+ * device buffers are owned by the caller (the Python side uses PyTorch only
+ * for allocation and streams); `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  Calls are asynchronous with respect to the host.
+ */
+#ifndef LEGO_B200_H
+#define LEGO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LEGO_ABI_VERSION 1
+
+/* Status codes map 1:1 onto the reference exception classes
+ * (errors.py:4-83) where one exists. */
+typedef enum {
+    LEGO_OK = 0,
+    LEGO_E_ARITY = 1,        /* ArityMismatch        */
+    LEGO_E_BOUNDS = 2,       /* OutOfBounds          */
+    LEGO_E_SHAPE = 3,        /* ShapeMismatch        */
+    LEGO_E_UNSUPPORTED = 4,  /* UnsupportedNode      */
+    LEGO_E_CUDA = 5,         /* CUDA runtime/driver  */
+    LEGO_E_NVRTC = 6,        /* kernel JIT failed    */
+    LEGO_E_BIJECTIVITY = 7,  /* BijectivityViolation */
+    LEGO_E_ARG = 8           /* invalid argument     */
+} lego_status;
+
+/* A loaded program: one generated layout lowering (index maps and/or a
+ * remap kernel) compiled for sm_100a. */
+typedef struct lego_program_s *lego_program;
+
+/* What a program holds; fixed at load time. */
+typedef enum {
+    LEGO_PROG_INDEX_MAP = 0,   /* lego_apply_map / lego_inv_map / lego_check_bijective */
+    LEGO_PROG_GATHER = 1,      /* remap: dst[f] = src[g(f)], per-element g             */
+    LEGO_PROG_TRANSPOSE = 2,   /* remap: digit-permutation, register-tiled transpose   */
+    LEGO_PROG_BAND = 3         /* remap: anti-diagonal band tiles through shared memory */
+} lego_program_kind;
+
+typedef struct {
+    int32_t kind;          /* lego_program_kind                                  */
+    int32_t elem_bytes;    /* remap element size (1, 2, 4, 8, 16); 0 for maps   */
+    int64_t n;             /* elements per matrix (map domain size)             */
+    int64_t units;         /* work units per matrix (vectors, warp tiles, bands) */
+    int32_t unit_threads;  /* threads per work unit (1 or 32)                   */
+    int32_t block;         /* threads per CTA                                   */
+    int32_t smem_bytes;    /* dynamic shared memory per CTA                     */
+    int32_t reserved;
+} lego_program_info;
+
+int32_t lego_abi_version(void);
+const char *lego_last_error(void);
+
+/* Device properties the host lowering needs (SM count, L2 bytes, CC). */
+lego_status lego_device_info(int32_t device, int32_t *sm_count, int64_t *l2_bytes,
+                             int32_t *cc_major, int32_t *cc_minor);
+
+/* --- kernel JIT: CUDA C++ text -> sm_100a cubin (NVRTC) ------------------ */
+/* Replaces reference emit.emit_expr(..., profile) (emit.py:90-102) as the
+ * last step of the lowering: the text is a generated device function spliced
+ * into a hand-written kernel template.  *cubin is freed with lego_free. */
+lego_status lego_nvrtc_compile(const char *source, size_t source_len, const char *arch,
+                               void **cubin, size_t *cubin_len, char *log, size_t log_cap);
+void lego_free(void *p);
+
+lego_status lego_program_load(const void *cubin, size_t cubin_len, const lego_program_info *info,
+                              lego_program *out);
+void lego_program_release(lego_program p);
+
+/* --- bulk layout evaluation ---------------------------------------------- */
+/* out[k] = apply(canon_unflatten(dims, first + k))  for k < count
+ *   (a loop of GroupBy.apply, layout.py:313; ExpandBy masks give -1)
+ * out_bytes = 4 (int32) or 8 (int64). */
+lego_status lego_apply_map(lego_program p, void *out, int32_t out_bytes, int64_t first,
+                           int64_t count, void *stream);
+/* out[k] = canon_flatten(dims, inv(first + k))  (a loop of GroupBy.inv, layout.py:320) */
+lego_status lego_inv_map(lego_program p, void *out, int32_t out_bytes, int64_t first,
+                         int64_t count, void *stream);
+/* Proves the layout's apply is a bijection onto [0, n) by a device-side
+ * histogram (validate() only checks GenPs up to 4096 points, layout.py:718).
+ * hist: caller scratch of n uint32; *violations (host) = number of positions
+ * hit != 1 times.  Synchronises the stream. */
+lego_status lego_check_bijective(lego_program p, uint32_t *hist, int64_t *violations,
+                                 void *stream);
+
+/* --- layout remap (the data movement the index maps describe) ------------- */
+/* For batch b < batch:  dst[b*dst_stride + f] = src[b*src_stride + g(f)]
+ * with g = src.apply o dst.inv compiled into the program, i.e. for every
+ * logical index x: dst[dst.apply(x)] = src[src.apply(x)].  Strides are in
+ * elements; buffers must be 16-byte aligned for the vector paths. */
+lego_status lego_remap(lego_program p, const void *src, void *dst, int64_t batch,
+                       int64_t src_stride, int64_t dst_stride, void *stream);
+
+/* --- fixed kernels with LEGO-derived layouts ------------------------------ */
+/* Row softmax, fp32, rows x cols row-major (cols % 4 == 0). */
+lego_status lego_softmax_f32(const float *x, float *y, int64_t rows, int64_t cols, void *stream);
+
+/* Needleman-Wunsch score matrix: score is (n+1) x (n+1) int32, row-major;
+ * sim is n x n; batch independent alignments back to back.
+ * S[0][j] = -j*p, S[i][0] = -i*p,
+ * S[i][j] = max(S[i-1][j-1] + sim[i-1][j-1], S[i-1][j] - p, S[i][j-1] - p).
+ * Tiles are swept in anti-diagonal order with the LEGO antidiag layout. */
+lego_status lego_nw_i32(const int32_t *sim, int32_t *score, int64_t n, int32_t penalty,
+                        int64_t batch, void *stream);
+
+/* bf16 GEMM on tcgen05/TMEM: C[b] = A[b] * B[b]^T-free layouts:
+ * A is M x K row-major, B is N x K row-major ("TN"), C is M x N row-major
+ * bf16, fp32 accumulation.  raster: 0 = row-major CTA order, 1 = LEGO
+ * grouped raster (GroupBy tile swizzle).  Requires M % 128 == 0,
+ * N % 256 == 0, K % 64 == 0. */
+lego_status lego_gemm_bf16(const void *A, const void *B, void *C, int64_t M, int64_t N,
+                           int64_t K, int64_t batch, int32_t raster, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEGO_B200_H */

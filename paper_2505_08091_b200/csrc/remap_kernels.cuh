@@ -1,0 +1,212 @@
+// remap_kernels.cuh -- hand-written sm_100a kernel templates for LEGO layouts.
+//
+// A program's source is:  lego_index.cuh + a generated `namespace gen { ... }`
+// (constants and device functions from paper_2505_08091_b200/codegen.py) +
+// this file with LEGO_KIND / LEGO_ELEM defined.  The generated functions are
+// the layout's index arithmetic (reference GroupBy.apply / inv,
+// pkg/src/lego/layout.py:313-328, lowered and simplified); the templates
+// own the memory access pattern.
+//
+//   LEGO_KIND 0  index maps:  lego_apply_map_*, lego_inv_map_*, lego_hist
+//   LEGO_KIND 1  gather:      dst[f] = src[g(f)]; 16-byte vector stores, and
+//                             16-byte vector loads when g is provably
+//                             contiguous over each vector (LEGO_CONTIG)
+//   LEGO_KIND 2  transpose:   g is a mixed-radix digit permutation whose
+//                             dst-innermost and src-innermost digits differ:
+//                             each lane moves a VxV micro-tile (V = 16/E) with
+//                             16-byte loads along src rows and 16-byte stores
+//                             along dst rows, transposed in registers
+//   LEGO_KIND 3  band:        anti-diagonal band tiles staged through smem
+#pragma once
+
+#define LEGO_GLOBAL extern "C" __global__
+
+struct lego_v16 { unsigned int w[4]; };
+
+static __device__ __forceinline__ lego_v16 lego_ld16(const unsigned char* p) {
+    lego_v16 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]) : "l"(p));
+    return v;
+}
+static __device__ __forceinline__ void lego_st16(unsigned char* p, const lego_v16& v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]) : "memory");
+}
+
+template <int E> struct lego_elem;
+template <> struct lego_elem<1> { typedef unsigned char t; };
+template <> struct lego_elem<2> { typedef unsigned short t; };
+template <> struct lego_elem<4> { typedef unsigned int t; };
+template <> struct lego_elem<8> { typedef unsigned long long t; };
+
+// ---------------------------------------------------------------------------
+#if LEGO_KIND == 0
+// index maps: one thread per output element, int32 or int64 outputs.
+template <typename T>
+static __device__ __forceinline__ void lego_map_body(T* out, long long first, long long count,
+                                                     int which) {
+    long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (; k < count; k += stride) {
+        long long v;
+        if (which == 0) { long long r; gen::apply_fn(first + k, r); v = r; }
+        else            { long long r; gen::inv_fn(first + k, r); v = r; }
+        out[k] = (T)v;
+    }
+}
+LEGO_GLOBAL void __launch_bounds__(256) lego_apply_map_i32(int* out, long long first, long long count) {
+    lego_map_body<int>(out, first, count, 0);
+}
+LEGO_GLOBAL void __launch_bounds__(256) lego_apply_map_i64(long long* out, long long first, long long count) {
+    lego_map_body<long long>(out, first, count, 0);
+}
+LEGO_GLOBAL void __launch_bounds__(256) lego_inv_map_i32(int* out, long long first, long long count) {
+    lego_map_body<int>(out, first, count, 1);
+}
+LEGO_GLOBAL void __launch_bounds__(256) lego_inv_map_i64(long long* out, long long first, long long count) {
+    lego_map_body<long long>(out, first, count, 1);
+}
+// histogram of apply over the whole logical space (bijectivity proof)
+LEGO_GLOBAL void __launch_bounds__(256) lego_hist(unsigned int* hist, long long count, long long n_out,
+                                                  unsigned long long* bad) {
+    long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (; k < count; k += stride) {
+        long long r;
+        gen::apply_fn(k, r);
+        if (r >= 0 && r < n_out) atomicAdd(hist + r, 1u);
+        else if (r != -1) atomicAdd(bad, 1ull);
+    }
+}
+LEGO_GLOBAL void __launch_bounds__(256) lego_hist_check(const unsigned int* hist, long long n,
+                                                        unsigned long long* bad) {
+    long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    unsigned long long local = 0;
+    for (; k < n; k += stride) local += (hist[k] != 1u);
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(bad, local);
+}
+#endif
+
+// ---------------------------------------------------------------------------
+#if LEGO_KIND == 1
+// gather: each thread owns VEC consecutive destination elements (16 bytes),
+// UNROLL vectors per thread with all loads issued before the stores.
+#define LEGO_VEC (16 / LEGO_ELEM)
+#ifndef LEGO_UNROLL
+#define LEGO_UNROLL 4
+#endif
+typedef lego_elem<LEGO_ELEM>::t lego_e;
+
+static __device__ __forceinline__ lego_v16 lego_gather_vec(const unsigned char* src, long long f) {
+    lego_v16 v;
+#if LEGO_CONTIG
+    long long s;
+    gen::src_of(f, s);
+    v = lego_ld16(src + s * LEGO_ELEM);
+#else
+    union { lego_e e[LEGO_VEC]; lego_v16 v; } u;
+#pragma unroll
+    for (int k = 0; k < LEGO_VEC; ++k) {
+        long long s;
+        gen::src_of(f + k, s);
+#if LEGO_MASKED
+        u.e[k] = s >= 0 ? __ldg(reinterpret_cast<const lego_e*>(src) + s) : (lego_e)0;
+#else
+        u.e[k] = __ldg(reinterpret_cast<const lego_e*>(src) + s);
+#endif
+    }
+    v = u.v;
+#endif
+    return v;
+}
+
+LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
+                                                   unsigned char* __restrict__ dst,
+                                                   long long src_stride, long long dst_stride) {
+    const unsigned char* s = src + (long long)blockIdx.y * src_stride * LEGO_ELEM;
+    unsigned char* d = dst + (long long)blockIdx.y * dst_stride * LEGO_ELEM;
+    const long long nvec = gen::N / LEGO_VEC;
+    const long long base = (long long)blockIdx.x * (blockDim.x * LEGO_UNROLL) + threadIdx.x;
+    lego_v16 v[LEGO_UNROLL];
+#pragma unroll
+    for (int u = 0; u < LEGO_UNROLL; ++u) {
+        const long long q = base + (long long)u * blockDim.x;
+        if (q < nvec) v[u] = lego_gather_vec(s, q * LEGO_VEC);
+    }
+#pragma unroll
+    for (int u = 0; u < LEGO_UNROLL; ++u) {
+        const long long q = base + (long long)u * blockDim.x;
+        if (q < nvec) lego_st16(d + q * 16, v[u]);
+    }
+}
+#endif
+
+// ---------------------------------------------------------------------------
+#if LEGO_KIND == 2
+// transpose of a digit permutation.  A warp owns a (4V) x (8V) tile: x runs
+// along the dst-innermost digit (dst stride 1, src stride gen::SX), y along
+// the src-innermost digit (src stride 1, dst stride gen::DY).  Lane (xg, yg)
+// = (lane / 8, lane % 8) loads V rows x = xg*V + r of V elements along y
+// (a 128-byte row segment per 8 lanes), transposes in registers and stores V
+// rows y = yg*V + c of V elements along x.
+#define LEGO_V (16 / LEGO_ELEM)
+
+static __device__ __forceinline__ unsigned int lego_word(const lego_v16& v, int i) { return v.w[i]; }
+
+static __device__ __forceinline__ void lego_transpose(const lego_v16 (&in)[LEGO_V], lego_v16 (&out)[LEGO_V]) {
+#if LEGO_ELEM == 4
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) out[c].w[r] = in[r].w[c];
+#elif LEGO_ELEM == 2
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+            out[c].w[w] = __byte_perm(in[2 * w].w[c >> 1], in[2 * w + 1].w[c >> 1],
+                                      (c & 1) ? 0x7632 : 0x5410);
+#elif LEGO_ELEM == 8
+    out[0].w[0] = in[0].w[0]; out[0].w[1] = in[0].w[1]; out[0].w[2] = in[1].w[0]; out[0].w[3] = in[1].w[1];
+    out[1].w[0] = in[0].w[2]; out[1].w[1] = in[0].w[3]; out[1].w[2] = in[1].w[2]; out[1].w[3] = in[1].w[3];
+#elif LEGO_ELEM == 1
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int sh = (c & 3) * 8;
+            const unsigned int b0 = (in[4 * w + 0].w[c >> 2] >> sh) & 0xffu;
+            const unsigned int b1 = (in[4 * w + 1].w[c >> 2] >> sh) & 0xffu;
+            const unsigned int b2 = (in[4 * w + 2].w[c >> 2] >> sh) & 0xffu;
+            const unsigned int b3 = (in[4 * w + 3].w[c >> 2] >> sh) & 0xffu;
+            out[c].w[w] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+        }
+#else
+    out[0] = in[0];
+#endif
+}
+
+LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
+                                                   unsigned char* __restrict__ dst,
+                                                   long long src_stride, long long dst_stride) {
+    const int lane = threadIdx.x & 31;
+    const long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (t >= gen::TILES) return;
+    const unsigned char* s = src + (long long)blockIdx.y * src_stride * LEGO_ELEM;
+    unsigned char* d = dst + (long long)blockIdx.y * dst_stride * LEGO_ELEM;
+    long long f0, s0;
+    gen::origin(t, f0, s0);
+    const int yg = lane & 7, xg = lane >> 3;
+    const unsigned char* sp = s + (s0 + (long long)(xg * LEGO_V) * gen::SX + yg * LEGO_V) * LEGO_ELEM;
+    lego_v16 rows[LEGO_V], cols[LEGO_V];
+#pragma unroll
+    for (int r = 0; r < LEGO_V; ++r) rows[r] = lego_ld16(sp + (long long)r * gen::SX * LEGO_ELEM);
+    lego_transpose(rows, cols);
+    unsigned char* dp = d + (f0 + (long long)(yg * LEGO_V) * gen::DY + xg * LEGO_V) * LEGO_ELEM;
+#pragma unroll
+    for (int c = 0; c < LEGO_V; ++c) lego_st16(dp + (long long)c * gen::DY * LEGO_ELEM, cols[c]);
+}
+#endif

@@ -1,0 +1,340 @@
+"""Bulk layout operations on B200 -- the backend's data-parallel hot path.
+
+The reference evaluates a layout one index at a time in Python
+(``GroupBy.apply``/``inv``, ``pkg/src/lego/layout.py:313-328``; ~10-15 us per
+element).  Here a layout is lowered once (:mod:`.lower`), its index
+arithmetic generated as CUDA (:mod:`.codegen`), spliced into a hand-written
+kernel template (``csrc/remap_kernels.cuh``), JIT-compiled for sm_100a by
+NVRTC (cubins cached on disk) and launched through the C ABI.
+
+Public operations (torch tensors in, torch tensors out, all on the GPU):
+
+* :func:`apply_map` / :func:`inv_map` -- a layout's bijection over its whole
+  index space (the reference's per-element ``apply`` / ``inv`` in bulk);
+* :func:`remap` (and :func:`gather` / :func:`scatter`) -- move a tensor from
+  one layout to another: for every logical index x,
+  ``dst[dst.apply(x)] = src[src.apply(x)]``;
+* :func:`check_bijective` -- prove a layout is a permutation on the device
+  (``validate`` only enumerates GenPs up to 4096 points);
+* :func:`softmax`, :func:`nw_score`, :func:`gemm` -- the fixed kernels.
+
+No function here computes on the CPU; without the native library they raise
+:class:`~.errors.BackendUnavailable`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import threading
+from typing import Dict, Optional, Tuple
+
+from . import codegen, lower, runtime
+from .errors import BijectivityViolation, ShapeMismatch, UnsupportedNode
+from .expr import Var
+
+CSRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc")
+_TEXT: Dict[str, str] = {}
+_PROGRAMS: Dict[tuple, runtime.Program] = {}
+_PLOCK = threading.Lock()
+
+# kernel launches issued through this module since import (for bench.py's
+# gpu_launches count; the driver cross-checks with the loaded .so list)
+LAUNCHES = [0]
+
+
+def _text(name: str) -> str:
+    if name not in _TEXT:
+        with open(os.path.join(CSRC, name)) as fh:
+            _TEXT[name] = fh.read()
+    return _TEXT[name]
+
+
+def _assemble(gen_body: str, defines: Dict[str, int]) -> str:
+    """Program source: helpers + generated namespace + kernel templates."""
+    head = "".join(f"#define {k} {v}\n" for k, v in defines.items())
+    return (head + _text("lego_index.cuh").replace("#pragma once", "") + "\nnamespace gen {\n"
+            + gen_body + "}\n" + _text("remap_kernels.cuh").replace("#pragma once", ""))
+
+
+def _layout_key(layout) -> tuple:
+    return (type(layout).__name__, layout) if layout is not None else ("row",)
+
+
+# ---------------------------------------------------------------------------
+# program builders
+# ---------------------------------------------------------------------------
+
+def _program(key, builder):
+    prog = _PROGRAMS.get(key)
+    if prog is None:
+        with _PLOCK:
+            prog = _PROGRAMS.get(key)
+            if prog is None:
+                source, info = builder()
+                prog = runtime.Program(runtime.compile_cubin(source), info, source)
+                _PROGRAMS[key] = prog
+    return prog
+
+
+def index_map_source(layout) -> Tuple[str, runtime.ProgramInfo]:
+    x, app = lower.apply_map_expr(layout)
+    injective = getattr(lower._group(layout), "injective", False)
+    body = codegen.constant("N", lower.logical_size(layout))
+    body += codegen.constant("M", lower.physical_size(layout))
+    body += codegen.generate("apply_fn", [x], {"out": app}).source
+    if injective:
+        body += "static __device__ __forceinline__ void inv_fn(const long long f, long long& out) { out = -1; }\n"
+    else:
+        f, inv = lower.inv_map_expr(layout)
+        body += codegen.generate("inv_fn", [f], {"out": inv}).source
+    info = runtime.ProgramInfo(kind=runtime.KIND_INDEX_MAP, elem_bytes=0,
+                               n=lower.logical_size(layout), units=lower.physical_size(layout),
+                               unit_threads=1, block=256, smem_bytes=0)
+    return _assemble(body, {"LEGO_KIND": 0}), info
+
+
+class RemapPlan:
+    """What the lowering decided for one (src layout, dst layout, elem size)."""
+
+    def __init__(self, kind, n_dst, n_src, elem_bytes, contig, masked, source, info, detail):
+        self.kind, self.n_dst, self.n_src = kind, n_dst, n_src
+        self.elem_bytes, self.contig, self.masked = elem_bytes, contig, masked
+        self.source, self.info, self.detail = source, info, detail
+
+    def __repr__(self):
+        names = {1: "gather", 2: "transpose", 3: "band"}
+        return (f"RemapPlan({names[self.kind]}, n={self.n_dst}, elem={self.elem_bytes}B, "
+                f"{self.detail})")
+
+
+def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
+    if elem_bytes not in (1, 2, 4, 8, 16):
+        raise UnsupportedNode(f"element size {elem_bytes} not supported (1, 2, 4, 8 or 16 bytes)")
+    f, g, n_dst, n_src = lower.gather_expr(src_layout, dst_layout)
+    lo, _hi = lower.value_range(g)
+    masked = lo < 0
+    vec = 16 // elem_bytes
+    if n_dst % vec:
+        raise UnsupportedNode(f"destination size {n_dst} is not a multiple of {vec} elements "
+                              f"({elem_bytes}-byte elements, 16-byte vectors)")
+    if not masked:
+        tp = lower.transpose_plan(g, f, n_dst, elem_bytes)
+        if tp is not None:
+            body = codegen.constant("N", n_dst) + codegen.constant("TILES", tp.tiles)
+            body += codegen.constant("SX", tp.sx) + codegen.constant("DY", tp.dy)
+            body += codegen.generate("origin", [tp.t], {"f0": tp.origin_f0,
+                                                        "s0": tp.origin_s0}).source
+            warps = 8
+            info = runtime.ProgramInfo(kind=runtime.KIND_TRANSPOSE, elem_bytes=elem_bytes, n=n_dst,
+                                       units=(tp.tiles + warps - 1) // warps, unit_threads=32,
+                                       block=32 * warps, smem_bytes=0)
+            src = _assemble(body, {"LEGO_KIND": 2, "LEGO_ELEM": elem_bytes})
+            return RemapPlan(runtime.KIND_TRANSPOSE, n_dst, n_src, elem_bytes, False, False, src,
+                             info, f"tile {tp.tx}x{tp.ty}, SX={tp.sx}, DY={tp.dy}")
+    width = 1 if masked else lower.contiguous_width(g, f, n_dst, widths=(vec,))
+    contig = width >= vec
+    body = codegen.constant("N", n_dst)
+    body += codegen.generate("src_of", [f], {"s": g}).source
+    unroll = 4
+    block = 256
+    nvec = n_dst // vec
+    units = (nvec + block * unroll - 1) // (block * unroll)
+    info = runtime.ProgramInfo(kind=runtime.KIND_GATHER, elem_bytes=elem_bytes, n=n_dst,
+                               units=units, unit_threads=1, block=block, smem_bytes=0)
+    src = _assemble(body, {"LEGO_KIND": 1, "LEGO_ELEM": elem_bytes, "LEGO_CONTIG": int(contig),
+                           "LEGO_MASKED": int(masked), "LEGO_UNROLL": unroll})
+    return RemapPlan(runtime.KIND_GATHER, n_dst, n_src, elem_bytes, contig, masked, src, info,
+                     f"contiguous={contig}, masked={masked}")
+
+
+def _remap_program(src_layout, dst_layout, elem_bytes):
+    key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes)
+    plan_box = {}
+
+    def build():
+        plan = plan_remap(src_layout, dst_layout, elem_bytes)
+        plan_box["plan"] = plan
+        return plan.source, plan.info
+
+    prog = _program(key, build)
+    return prog
+
+
+def _map_program(layout):
+    return _program(("map", _layout_key(layout)), lambda: index_map_source(layout))
+
+
+# ---------------------------------------------------------------------------
+# public operations
+# ---------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    return torch
+
+
+def _device(device):
+    torch = _torch()
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def apply_map(layout, *, dtype=None, device=None, first: int = 0, count: Optional[int] = None,
+              out=None, stream=None):
+    """``out[k] = layout.apply(canon_unflatten(dims, first + k))`` on the GPU
+    (ExpandBy masked positions are -1)."""
+    torch = _torch()
+    n = lower.logical_size(layout)
+    count = n - first if count is None else count
+    prog = _map_program(layout)
+    if out is None:
+        dtype = dtype or (torch.int32 if lower.physical_size(layout) < 2 ** 31 else torch.int64)
+        out = torch.empty(count, dtype=dtype, device=_device(device))
+    runtime.check(runtime.lib().lego_apply_map(prog.handle, out.data_ptr(), out.element_size(),
+                                               first, count, runtime.stream_handle(stream)),
+                  "lego_apply_map")
+    LAUNCHES[0] += 1
+    return out
+
+
+def inv_map(layout, *, dtype=None, device=None, first: int = 0, count: Optional[int] = None,
+            out=None, stream=None):
+    """``out[k] = canon_flatten(dims, layout.inv(first + k))`` on the GPU."""
+    torch = _torch()
+    n = lower.physical_size(layout)
+    count = n - first if count is None else count
+    prog = _map_program(layout)
+    if out is None:
+        dtype = dtype or (torch.int32 if lower.logical_size(layout) < 2 ** 31 else torch.int64)
+        out = torch.empty(count, dtype=dtype, device=_device(device))
+    runtime.check(runtime.lib().lego_inv_map(prog.handle, out.data_ptr(), out.element_size(),
+                                             first, count, runtime.stream_handle(stream)),
+                  "lego_inv_map")
+    LAUNCHES[0] += 1
+    return out
+
+
+def check_bijective(layout, *, device=None, stream=None, raise_on_failure: bool = False) -> bool:
+    """Device-side proof that ``apply`` hits every position exactly once."""
+    torch = _torch()
+    prog = _map_program(layout)
+    hist = torch.empty(lower.physical_size(layout), dtype=torch.int32, device=_device(device))
+    bad = runtime.I64()
+    runtime.check(runtime.lib().lego_check_bijective(prog.handle, hist.data_ptr(), ctypes.byref(bad),
+                                                     runtime.stream_handle(stream)),
+                  "lego_check_bijective")
+    LAUNCHES[0] += 2
+    ok = bad.value == 0
+    if not ok and raise_on_failure:
+        raise BijectivityViolation(f"{bad.value} positions are not hit exactly once")
+    return ok
+
+
+def remap_plan(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
+    """The lowering decision (kernel family, geometry) without compiling."""
+    return plan_remap(src_layout, dst_layout, elem_bytes)
+
+
+def remap(src, src_layout=None, dst_layout=None, *, out=None, stream=None):
+    """Move ``src`` (shape ``(..., n_src)``) into the destination layout:
+    for every logical index x, ``out[..., dst.apply(x)] = src[..., src.apply(x)]``.
+    ``None`` on either side means row-major over the other side's dims."""
+    torch = _torch()
+    if not src.is_cuda:
+        raise ShapeMismatch("remap takes a CUDA tensor (no CPU path)")
+    elem = src.element_size()
+    f_dst = lower.physical_size(dst_layout) if dst_layout is not None else lower.logical_size(src_layout)
+    n_src = lower.physical_size(src_layout) if src_layout is not None else lower.logical_size(dst_layout)
+    if src.numel() % n_src:
+        raise ShapeMismatch(f"source of {src.numel()} elements is not a batch of layouts of "
+                            f"size {n_src}")
+    src = src.contiguous()
+    batch = src.numel() // n_src
+    batch_shape = tuple(src.shape[:-1]) if src.dim() and src.shape[-1] == n_src else (batch,)
+    if out is None:
+        out = torch.empty(*batch_shape, f_dst, dtype=src.dtype, device=src.device)
+    prog = _remap_program(src_layout, dst_layout, elem)
+    st = runtime.stream_handle(stream)
+    done = 0
+    while done < batch or (batch == 0 and done == 0):
+        if batch == 0:
+            break
+        b = min(65535, batch - done)
+        runtime.check(runtime.lib().lego_remap(
+            prog.handle, src.data_ptr() + done * n_src * elem, out.data_ptr() + done * f_dst * elem,
+            b, n_src, f_dst, st), "lego_remap")
+        LAUNCHES[0] += 1
+        done += b
+    return out
+
+
+def gather(src, layout, **kw):
+    """Physical buffer in ``layout`` -> logical row-major order."""
+    return remap(src, layout, None, **kw)
+
+
+def scatter(src, layout, **kw):
+    """Logical row-major data -> physical buffer in ``layout``."""
+    return remap(src, None, layout, **kw)
+
+
+# ---------------------------------------------------------------------------
+# fixed kernels
+# ---------------------------------------------------------------------------
+
+def softmax(x, *, out=None, stream=None):
+    """Row softmax over the last dim of a contiguous fp32 CUDA tensor."""
+    torch = _torch()
+    if x.dtype != torch.float32 or not x.is_cuda:
+        raise ShapeMismatch("softmax takes a CUDA float32 tensor")
+    x = x.contiguous()
+    cols = x.shape[-1]
+    rows = x.numel() // cols if cols else 0
+    out = torch.empty_like(x) if out is None else out
+    runtime.check(runtime.lib().lego_softmax_f32(x.data_ptr(), out.data_ptr(), rows, cols,
+                                                 runtime.stream_handle(stream)), "lego_softmax_f32")
+    LAUNCHES[0] += 1
+    return out
+
+
+def nw_score(sim, penalty: int, *, out=None, stream=None):
+    """Needleman-Wunsch score matrices for int32 similarity ``(..., n, n)``."""
+    torch = _torch()
+    if sim.dtype != torch.int32 or not sim.is_cuda or sim.shape[-1] != sim.shape[-2]:
+        raise ShapeMismatch("nw_score takes a CUDA int32 tensor of shape (..., n, n)")
+    sim = sim.contiguous()
+    n = sim.shape[-1]
+    batch = sim.numel() // (n * n) if n else 0
+    if out is None:
+        out = torch.empty(*sim.shape[:-2], n + 1, n + 1, dtype=torch.int32, device=sim.device)
+    runtime.check(runtime.lib().lego_nw_i32(sim.data_ptr(), out.data_ptr(), n, int(penalty), batch,
+                                            runtime.stream_handle(stream)), "lego_nw_i32")
+    LAUNCHES[0] += 1
+    return out
+
+
+def gemm(a, b, *, out=None, raster: int = 1, stream=None):
+    """``C = A @ B.T`` for bf16 ``A (..., M, K)`` and ``B (..., N, K)`` on tcgen05."""
+    torch = _torch()
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or not a.is_cuda:
+        raise ShapeMismatch("gemm takes CUDA bfloat16 tensors")
+    a, b = a.contiguous(), b.contiguous()
+    M, K = a.shape[-2], a.shape[-1]
+    N = b.shape[-2]
+    if b.shape[-1] != K:
+        raise ShapeMismatch(f"inner dims differ: {K} vs {b.shape[-1]}")
+    batch = a.numel() // (M * K)
+    if out is None:
+        out = torch.empty(*a.shape[:-2], M, N, dtype=torch.bfloat16, device=a.device)
+    runtime.check(runtime.lib().lego_gemm_bf16(a.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K,
+                                               batch, raster, runtime.stream_handle(stream)),
+                  "lego_gemm_bf16")
+    LAUNCHES[0] += 1
+    return out
+
+
+def _ensure_var(v) -> Var:
+    return v

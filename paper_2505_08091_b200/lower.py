@@ -1,0 +1,275 @@
+"""Lowering of layouts to kernel plans (the step between the algebra and CUDA).
+
+Builds the index expressions the kernels need directly from the layout's own
+``apply``/``inv`` (reference ``layout.py:313-328``), composing stage by stage
+on *flat* positions so that the canonical flatten/unflatten pair around the
+logical index cancels instead of surviving as div/mod chains, then picks the
+kernel family by *proving* structural facts about the simplified map:
+
+* ``contiguous_width`` -- g(w*q + r) - g(w*q) - r simplifies to 0, i.e. every
+  aligned run of w destination elements reads w consecutive source elements
+  (16-byte vector loads are then exact);
+* ``digit_terms`` -- g is a permutation of mixed-radix digits of f
+  (``sum(((f // lo) % span) * stride)`` with the digit ranges tiling
+  ``[1, n)``), which licenses the register-tiled transpose: the tile geometry
+  and the tile-origin function are derived from the digits.
+
+Everything here is host-side and runs once per (layout pair, element size);
+the results are cached by :mod:`.kernels`.
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Optional, Tuple
+
+from .errors import ArityMismatch, ShapeMismatch
+from .expr import (
+    Add,
+    And,
+    Call,
+    Cmp,
+    Expr,
+    FloorDiv,
+    IntConst,
+    Mod,
+    Mul,
+    Select,
+    Sub,
+    Var,
+    VarRange,
+    as_expr,
+)
+from .layout import ExpandBy, GroupBy, canon_flatten, canon_unflatten
+from .simplify import Intervals, _digit_of, _lin_of, simplify
+
+
+def substitute(e: Expr, env: Dict[str, Expr]) -> Expr:
+    """Replace variables by expressions (DAG-aware, memoised)."""
+    memo: Dict[Expr, Expr] = {}
+
+    def sub(n):
+        got = memo.get(n)
+        if got is not None:
+            return got
+        t = type(n)
+        if t is Var:
+            out = env.get(n.name, n)
+        elif t is IntConst:
+            out = n
+        elif t in (Add, Sub, Mul):
+            out = t(sub(n.lhs), sub(n.rhs))
+        elif t in (FloorDiv, Mod):
+            out = t(sub(n.num), sub(n.den))
+        elif t is Select:
+            out = Select(cond(n.cond), sub(n.then), sub(n.orelse))
+        elif t is Call:
+            out = Call(n.intrinsic, tuple(sub(a) for a in n.args))
+        else:
+            raise TypeError(n)
+        memo[n] = out
+        return out
+
+    def cond(c):
+        if type(c) is Cmp:
+            return Cmp(c.op, sub(c.lhs), sub(c.rhs))
+        return And(cond(c.lhs), cond(c.rhs))
+
+    return sub(e)
+
+
+# ---------------------------------------------------------------------------
+# Flat maps.
+# ---------------------------------------------------------------------------
+
+def _group(layout):
+    return layout.inner if isinstance(layout, ExpandBy) else layout
+
+
+def logical_size(layout) -> int:
+    return math.prod(layout.dims)
+
+
+def physical_size(layout) -> int:
+    return layout.size
+
+
+def apply_flat(layout, x: Expr) -> Expr:
+    """Position of the logical element whose row-major flat index is x:
+    ``layout.apply(canon_unflatten(dims, x))`` with the leading
+    flatten(unflatten(x)) = x cancelled."""
+    g = _group(layout)
+    g._check()
+    pos = x
+    for stage in g.orders:
+        pos = stage.apply(canon_unflatten(stage.dims, pos))
+    if isinstance(layout, ExpandBy):
+        layout._check()
+        coords = canon_unflatten(layout.expanded, pos)
+        phys = canon_flatten(layout.physical, coords, check=False)
+        from .expr import and_all, lt
+        pos = Select(and_all(lt(c, n) for c, n in zip(coords, layout.physical)), phys,
+                     IntConst(-1))
+    return pos
+
+
+def inv_flat(layout, f: Expr) -> Expr:
+    """Row-major flat logical index of the element at position f:
+    ``canon_flatten(dims, layout.inv(f))`` with the trailing pair cancelled."""
+    pos = f
+    if isinstance(layout, ExpandBy):
+        layout._check()
+        pos = canon_flatten(layout.expanded, canon_unflatten(layout.physical, pos), check=False)
+    g = _group(layout)
+    if g.injective:
+        from .errors import LegoError
+        raise LegoError("injective layout exports apply only, not inv")
+    g._check()
+    for stage in g.orders[::-1]:
+        pos = canon_flatten(stage.dims, stage.inv(pos), check=False)
+    return pos
+
+
+def flat_var(name: str, n: int) -> Var:
+    return Var(name, VarRange(0, n))
+
+
+def apply_map_expr(layout) -> Tuple[Var, Expr]:
+    x = flat_var("x", logical_size(layout))
+    return x, simplify(as_expr(apply_flat(layout, x)))
+
+
+def inv_map_expr(layout) -> Tuple[Var, Expr]:
+    f = flat_var("f", physical_size(layout))
+    return f, simplify(as_expr(inv_flat(layout, f)))
+
+
+def check_pair(src_layout, dst_layout):
+    if src_layout is None and dst_layout is None:
+        raise ShapeMismatch("remap needs at least one layout")
+    if src_layout is not None and dst_layout is not None:
+        if tuple(src_layout.dims) != tuple(dst_layout.dims):
+            raise ArityMismatch(f"source layout dims {tuple(src_layout.dims)} differ from "
+                                f"destination dims {tuple(dst_layout.dims)}")
+
+
+def gather_expr(src_layout, dst_layout) -> Tuple[Var, Expr, int, int]:
+    """g with dst[f] = src[g(f)]: g = src.apply o dst.inv (row-major where a
+    side is None).  Returns (f, g, dst size, src size)."""
+    check_pair(src_layout, dst_layout)
+    some = src_layout if src_layout is not None else dst_layout
+    n_dst = physical_size(dst_layout) if dst_layout is not None else logical_size(some)
+    n_src = physical_size(src_layout) if src_layout is not None else logical_size(some)
+    f = flat_var("f", n_dst)
+    x = inv_flat(dst_layout, f) if dst_layout is not None else f
+    s = apply_flat(src_layout, as_expr(x)) if src_layout is not None else x
+    return f, simplify(as_expr(s)), n_dst, n_src
+
+
+# ---------------------------------------------------------------------------
+# Structural proofs.
+# ---------------------------------------------------------------------------
+
+def contiguous_width(g: Expr, f: Var, n: int, widths=(16, 8, 4, 2)) -> int:
+    """Largest w in widths such that g(w*q + r) == g(w*q) + r for all q, r."""
+    for w in widths:
+        if n % w:
+            continue
+        q = Var("q", VarRange(0, n // w))
+        r = Var("r", VarRange(0, w))
+        lhs = substitute(g, {f.name: q * w + r})
+        rhs = substitute(g, {f.name: q * w})
+        if simplify(lhs - rhs - r) == IntConst(0):
+            return w
+    return 1
+
+
+def digit_terms(g: Expr, f: Var, n: int) -> Optional[List[Tuple[int, int, int]]]:
+    """If g == sum(((f // lo) % span) * stride) with digit runs tiling [1, n),
+    return [(lo, span, stride)] sorted by lo; else None."""
+    lin = _lin_of(g)
+    if lin.const != 0:
+        return None
+    digits = []
+    for atom, coef in lin.terms.items():
+        base, lo, span = _digit_of(atom)
+        if base is None or base != f:
+            return None
+        if span is None:
+            if n % lo:
+                return None
+            span = n // lo
+        digits.append((lo, span, coef))
+    digits.sort()
+    expect = 1
+    for lo, span, _ in digits:
+        if lo != expect:
+            return None
+        expect = lo * span
+    if expect != n:
+        return None
+    return digits
+
+
+def split_digit(digits, lo_target: int, inner: int):
+    """Split the digit at lo_target into (inner) and (span // inner) parts."""
+    out = []
+    for lo, span, stride in digits:
+        if lo == lo_target and span > inner:
+            out.append((lo, inner, stride))
+            out.append((lo * inner, span // inner, stride * inner))
+        else:
+            out.append((lo, span, stride))
+    return out
+
+
+class TransposePlan:
+    def __init__(self, tiles: int, sx: int, dy: int, origin_f0: Expr, origin_s0: Expr, t: Var,
+                 tx: int, ty: int):
+        self.tiles, self.sx, self.dy = tiles, sx, dy
+        self.origin_f0, self.origin_s0, self.t = origin_f0, origin_s0, t
+        self.tx, self.ty = tx, ty
+
+
+def transpose_plan(g: Expr, f: Var, n: int, elem_bytes: int) -> Optional[TransposePlan]:
+    """Register-tiled transpose geometry for a digit-permutation gather."""
+    if 16 % elem_bytes:
+        return None
+    digits = digit_terms(g, f, n)
+    if digits is None:
+        return None
+    v = 16 // elem_bytes
+    tx, ty = 4 * v, 8 * v                 # warp tile: x along dst digit, y along src digit
+    x_lo, x_span, sx = digits[0]
+    if sx == 1:
+        return None                        # contiguous: the gather path is better
+    ydig = [d for d in digits if d[2] == 1]
+    if len(ydig) != 1:
+        return None
+    y_lo, y_span, _ = ydig[0]
+    if x_span % tx or y_span % ty or sx % v:
+        return None
+    # every other digit must keep 16-byte alignment on both sides
+    for lo, span, stride in digits:
+        if (lo, span) in ((x_lo, x_span), (y_lo, y_span)):
+            continue
+        if stride % v or lo % v:
+            return None
+    # tile index t -> (x_hi fastest, mid, y_hi, hi) -> dst origin f0
+    x_hi = x_span // tx
+    mid = y_lo // x_span
+    y_hi = y_span // ty
+    hi = n // (y_lo * y_span)
+    tiles = x_hi * mid * y_hi * hi
+    t = Var("t", VarRange(0, tiles))
+    c0 = t % x_hi
+    c1 = (t // x_hi) % mid
+    c2 = (t // (x_hi * mid)) % y_hi
+    c3 = t // (x_hi * mid * y_hi)
+    f0 = simplify(c0 * tx + c1 * x_span + c2 * (ty * y_lo) + c3 * (y_lo * y_span))
+    s0 = simplify(substitute(g, {f.name: f0}))
+    return TransposePlan(tiles, sx, y_lo, f0, s0, t, tx, ty)
+
+
+def value_range(e: Expr):
+    return Intervals().of(e)

@@ -468,6 +468,22 @@ class _Normaliser:
             return self.mod_rest(rest, d)
         return self.finish_sum(quot.add(_lin_of(self.div_rest(rest, d))))
 
+    def split_small(self, rest: Lin, d: int):
+        """Find a | d with rest = a*Q + R where every term of Q has a
+        coefficient divisible by a and 0 <= R < a.  Then (floor semantics,
+        any sign of Q):  rest // d == Q // (d/a)  and
+        rest % d == a*(Q % (d/a)) + R.  Returns (a, Q, R) or None."""
+        cands = sorted({math.gcd(d, c) for c in rest.terms.values()} - {1, d}, reverse=True)
+        for a in cands:
+            big = Lin({t: c // a for t, c in rest.terms.items() if c % a == 0}, 0)
+            small = Lin({t: c for t, c in rest.terms.items() if c % a != 0}, rest.const)
+            if not big.terms:
+                continue
+            r = self.lin_interval(small)
+            if r is not None and r[0] >= 0 and r[1] < a:
+                return a, big, small
+        return None
+
     def div_rest(self, rest: Lin, d: int) -> Expr:
         if d == 1:
             return _build(rest)
@@ -476,6 +492,10 @@ class _Normaliser:
             return IntConst(r[0] // d)
         if rest.is_const():
             return IntConst(rest.const // d)
+        sp = self.split_small(rest, d)
+        if sp is not None:
+            a, big, _ = sp
+            return self.div_mod(True, _build(big), d // a)
         if len(rest.terms) == 1 and rest.const == 0:
             (a, c), = rest.terms.items()
             if c == 1:
@@ -496,6 +516,11 @@ class _Normaliser:
             return _build(rest)
         if rest.is_const():
             return IntConst(rest.const % d)
+        sp = self.split_small(rest, d)
+        if sp is not None:
+            a, big, small = sp
+            hi = _lin_of(self.div_mod(False, _build(big), d // a)).scaled(a)
+            return self.finish_sum(hi.add(small))
         if len(rest.terms) == 1 and rest.const == 0:
             (a, c), = rest.terms.items()
             if c == 1 and type(a) is Mod and type(a.den) is IntConst:
