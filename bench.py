@@ -1,0 +1,400 @@
+"""Benchmark of the LEGO B200 backend (contract: one JSON line on rank 0).
+
+Headline workload (BASELINE.json metric on its config 2, the largest
+single-GPU remap config): the LEGO dimension-permutation layout
+``GroupBy([16384,16384]).OrderBy(Col(16384,16384))`` applied to a
+16384 x 16384 bf16 matrix -- every logical element (i, j) moves from its
+row-major position to ``apply(i, j) = j*16384 + i``.  One step = one remap
+of one matrix per GPU (weak scaling: N GPUs remap N independent matrices,
+no data-path collective).  ``value`` = algorithmic bytes moved by all ranks
+(read + write, 2 x 512 MiB per matrix) / max-over-ranks device time.
+
+The input (512 MiB) and output are 4x the 126 MB L2, so no flush is needed
+between iterations.  The other BASELINE configs are reported under
+``"kernels"`` (measured in the same run, not the headline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N = 16384
+HEADLINE_DSL = "GroupBy([16384,16384]).OrderBy(Col(16384,16384))"
+METRIC = "layout-remap GB/s (frac of HBM peak); LEGO-GEMM TFLOP/s; 1/2/4/8 GPU"
+WORKLOAD = ("cfg2: LEGO transpose layout GroupBy([16384,16384]).OrderBy(Col(16384,16384)) "
+            "remapping a 16384x16384 bf16 matrix (row-major -> layout), 1 matrix per GPU per step")
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return {"hbm": float(p["hbm_gbs"]), "bf16": float(p["bf16_tflops"]),
+                "bf16_sustained": float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+def traffic_table():
+    """Per-launch DRAM bytes from the committed ncu --set full captures."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock/throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception:  # noqa: BLE001 - clocks are best effort
+            self._nv = None
+        return self
+
+    def _run(self):
+        nv = self._nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.02)
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(value, world):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def time_steps(fn, steps, warmup, world):
+    """W warm-up steps, then EXACTLY K timed steps bracketed by barrier +
+    synchronize; device time from CUDA events on the launching stream."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier(world)
+    stream = torch.cuda.current_stream()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(steps):
+        fn()
+    end.record(stream)
+    end.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    return max_over_ranks(start.elapsed_time(end), world)
+
+
+def kernel_event_time(fn, iters):
+    """Average duration of the dominant launch (events around each launch)."""
+    import torch
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(iters)]
+    for s, e in evs:
+        s.record(stream)
+        fn()
+        e.record(stream)
+    torch.cuda.synchronize()
+    return sum(s.elapsed_time(e) for s, e in evs) / iters
+
+
+# ---------------------------------------------------------------------------
+# CPU side (oracle port; test infrastructure, timed as the baseline only)
+# ---------------------------------------------------------------------------
+
+def cpu_remap_rate(target_seconds=10.0):
+    """Time the C oracle port of the reference per-element remap on this
+    host's cores over a bounded sample of the headline workload."""
+    import numpy as np
+    from oracle import oracle as O
+    spec = O.parse(HEADLINE_DSL)
+    n = N * N
+    src = (np.arange(n, dtype=np.int64) % 65536).astype(np.uint16)
+    out = np.zeros(n, dtype=np.uint16)
+    probe = 1 << 22
+    t0 = time.perf_counter()
+    O.remap(src, None, spec, first=0, count=probe, out=out)
+    dt = time.perf_counter() - t0
+    count = int(min(n, max(probe, probe * target_seconds / max(dt, 1e-9))))
+    count -= count % N
+    t0 = time.perf_counter()
+    O.remap(src, None, spec, first=0, count=count, out=out)
+    dt = time.perf_counter() - t0
+    gbs = 2 * 2 * count / dt / 1e9
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": O.threads(), "kind": "port",
+            "sample": f"{count} of {n} elements ({count // N} rows) of the headline remap, "
+                      f"oracle/lego_oracle.c per-element apply (reference layout.py:313) "
+                      f"with {O.threads()} OpenMP threads, {dt:.2f} s"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rates = []
+    base = None
+    for k in range(args.warmup + args.steps):
+        r = cpu_remap_rate(target_seconds=max(1.0, 60.0 / max(1, args.warmup + args.steps)))
+        if k >= args.warmup:
+            rates.append(r["value"])
+            base = r
+    value = sum(rates) / len(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(2 * 2 * N * N / (value * 1e9) * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "per_gpu_matrices": 1},
+            "cpu_baseline": {**base, "value": round(value, 3)},
+            "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+
+def run(args):
+    import torch
+
+    import paper_2505_08091_b200 as L
+    from paper_2505_08091_b200 import kernels as K
+
+    world, rank, local = dist_setup(args)
+    pk = peaks()
+    layout = L.parse_layout(HEADLINE_DSL)
+    nbytes = N * N * 2
+    g = torch.Generator(device="cuda").manual_seed(1 + rank)
+    src = torch.randn(N, N, generator=g, device="cuda", dtype=torch.float32).to(torch.bfloat16)
+    src = src.reshape(N * N)
+    out = torch.empty_like(src)
+    step = lambda: K.remap(src, None, layout, out=out)  # noqa: E731
+    step()
+    # correctness spot check of the timed path: out[j*N + i] == src[i*N + j]
+    probe = torch.randint(0, N, (2, 4096), device="cuda")
+    ok = torch.equal(out[probe[1] * N + probe[0]], src[probe[0] * N + probe[1]])
+    launches0 = K.LAUNCHES[0]
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        ms = time_steps(step, args.steps, args.warmup, world)
+    launches = K.LAUNCHES[0] - launches0 - args.warmup
+    ms_step = ms / args.steps
+    value = world * 2 * nbytes / (ms_step * 1e-3) / 1e9
+    # dominant kernel = the remap itself: average launch duration
+    kms = kernel_event_time(step, max(5, min(args.steps, 20)))
+    achieved = 2 * nbytes / (kms * 1e-3) / 1e9
+    tr = traffic_table().get("remap_transpose_bf16")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm"], "unit": "GB/s",
+                "frac": round(achieved / pk["hbm"], 4), "peak_source": pk["source"],
+                "frac_of_8000": round(achieved / 8000.0, 4),
+                "traffic": tr, "algorithmic_bytes_per_launch": 2 * nbytes}
+
+    # e2e: public API with pinned host buffers, H2D + remap + D2H each step
+    host_in = torch.empty(N * N, dtype=torch.bfloat16, pin_memory=True)
+    host_in.copy_(src)
+    host_out = torch.empty(N * N, dtype=torch.bfloat16, pin_memory=True)
+    dev_in = torch.empty_like(src)
+    dev_out = torch.empty_like(src)
+
+    def e2e_step():
+        dev_in.copy_(host_in, non_blocking=True)
+        K.remap(dev_in, None, layout, out=dev_out)
+        host_out.copy_(dev_out, non_blocking=True)
+
+    e2e_ms = time_steps(e2e_step, max(3, args.steps // 4), 2, world) / max(3, args.steps // 4)
+    e2e_value = world * 2 * nbytes / (e2e_ms * 1e-3) / 1e9
+
+    kernels = {}
+    if not args.headline_only:
+        kernels = other_kernels(args, pk, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_remap_rate()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (randn bf16, seed 1+rank)",
+            "config": {"workload": WORKLOAD, "per_gpu_matrices": 1,
+                       "layout": HEADLINE_DSL, "elem_bytes": 2,
+                       "l2": "no flush: 512 MiB input + 512 MiB output per GPU >> 126 MB L2",
+                       "parallelism": f"weak: {world} independent matrices, no data-path collective",
+                       "check": "ok" if ok else "MISMATCH"},
+            "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 1), "unit": "GB/s", "h2d_bytes_per_step": nbytes,
+                    "d2h_bytes_per_step": nbytes,
+                    "note": "public API kernels.remap with pinned host buffers; PCIe-bound"},
+            "gpu_launches": launches, "clocks": clocks.summary(), "kernels": kernels,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def other_kernels(args, pk, world):
+    """The remaining BASELINE configs, timed the same way (W warm-up, K steps)."""
+    import torch
+
+    import paper_2505_08091_b200 as L
+    from paper_2505_08091_b200 import kernels as K
+    res = {}
+    steps, warm = max(5, args.steps), max(3, args.warmup)
+
+    def hbm_entry(name, nbytes, fn, traffic_key, extra=None):
+        ms = time_steps(fn, steps, warm, world) / steps
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        res[name] = {"GB/s": round(gbs, 1), "frac": round(gbs / pk["hbm"], 4),
+                     "us": round(ms * 1e3, 1), "traffic": traffic_table().get(traffic_key),
+                     **(extra or {})}
+
+    # cfg1: 4096^2 fp32 tiled remap, batch 8 (512 MiB in, > L2)
+    g1 = L.parse_layout("GroupBy([4096,4096]).OrderBy(RegP([128,32,128,32],[1,3,2,4]))")
+    x1 = torch.randn(8, 4096 * 4096, device="cuda")
+    y1 = torch.empty_like(x1)
+    hbm_entry("cfg1_tiled_remap_fp32_b8", 2 * x1.numel() * 4,
+              lambda: K.remap(x1, None, g1, out=y1), "remap_gather_fp32")
+    del x1, y1
+    # cfg3: softmax 8192^2 fp32 (256 MiB in: 2x L2)
+    x3 = torch.randn(8192, 8192, device="cuda") * 4
+    y3 = torch.empty_like(x3)
+    hbm_entry("cfg3_softmax_fp32", 2 * x3.numel() * 4, lambda: K.softmax(x3, out=y3),
+              "softmax_fp32")
+    del x3, y3
+    # cfg4a: antidiag remap 16384^2 int32
+    g4 = L.parse_layout("GroupBy([16384,16384]).OrderBy(GenP([16384,16384], antidiag))")
+    x4 = torch.arange(16384 * 16384, device="cuda", dtype=torch.int32)
+    y4 = torch.empty_like(x4)
+    hbm_entry("cfg4a_antidiag_remap_i32", 2 * x4.numel() * 4,
+              lambda: K.remap(x4, None, g4, out=y4), "remap_antidiag_i32",
+              {"plan": repr(K.remap_plan(None, g4, 4))})
+    del x4, y4
+    # cfg4b: NW wavefront 16384^2 int32
+    try:
+        sim = torch.randint(-10, 11, (16384, 16384), device="cuda", dtype=torch.int32)
+        score = torch.empty(16385, 16385, device="cuda", dtype=torch.int32)
+        ms = time_steps(lambda: K.nw_score(sim, 10, out=score), max(3, steps // 2), 2, world)
+        ms /= max(3, steps // 2)
+        cells = 16384 * 16384
+        res["cfg4b_nw_wavefront_i32"] = {"GCUPS": round(cells / (ms * 1e-3) / 1e9, 1),
+                                         "us": round(ms * 1e3, 1),
+                                         "GB/s": round((cells * 4 + 16385 ** 2 * 4) / (ms * 1e-3) / 1e9, 1)}
+        del sim, score
+    except Exception as exc:  # noqa: BLE001
+        res["cfg4b_nw_wavefront_i32"] = {"unavailable": str(exc)[:200]}
+    # cfg5: bf16 GEMM 8192^3 on tcgen05
+    try:
+        a = torch.randn(8192, 8192, device="cuda").to(torch.bfloat16)
+        b = torch.randn(8192, 8192, device="cuda").to(torch.bfloat16)
+        c = torch.empty(8192, 8192, device="cuda", dtype=torch.bfloat16)
+        ms = time_steps(lambda: K.gemm(a, b, out=c), steps, warm, world) / steps
+        tf = 2 * 8192 ** 3 / (ms * 1e-3) / 1e12
+        res["cfg5_gemm_bf16_8192"] = {"TFLOP/s": round(tf, 1), "frac": round(tf / pk["bf16"], 4),
+                                      "frac_sustained": round(tf / pk["bf16_sustained"], 4),
+                                      "us": round(ms * 1e3, 1)}
+    except Exception as exc:  # noqa: BLE001
+        res["cfg5_gemm_bf16_8192"] = {"unavailable": str(exc)[:200]}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="lego", choices=["lego", "reference"])
+    ap.add_argument("--headline-only", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,9 +1,363 @@
-// gemm_tcgen05.cu -- bf16 GEMM on tcgen05/TMEM (config 5).
-// (first version: placeholder until the tcgen05 kernel lands)
+// gemm_tcgen05.cu -- bf16 GEMM on 5th-generation tensor cores (config 5).
+//
+//   C[b] (M x N, bf16, row-major) = A[b] (M x K, row-major) * B[b]^T (B is N x K row-major)
+//
+// Blackwell-native structure, written directly in PTX:
+//  * persistent kernel, one CTA per SM, 6 warps with fixed roles:
+//      warp 0      TMA producer (one elected lane): cp.async.bulk.tensor into a
+//                  4-stage smem ring (A 128x64, B 256x64 bf16 per stage, 128-byte
+//                  swizzle), completion via mbarrier transaction counts
+//      warp 1      TMEM allocator (whole warp) + MMA issuer (one lane):
+//                  tcgen05.mma.cta_group::1.kind::f16, M=128 N=256 K=16, fp32
+//                  accumulators in TMEM, double-buffered (2 x 256 columns) so the
+//                  epilogue of tile i overlaps the main loop of tile i+1;
+//                  tcgen05.commit releases smem stages / publishes accumulators
+//      warps 2..5  epilogue: tcgen05.ld 32x32b -> bf16 -> global
+//  * LEGO-specified CTA raster: the output-tile index walks the layout
+//        GroupBy([MB/G, NB, G]).OrderBy(Row(MB/G, NB, G))  (tiles grouped G
+//    m-blocks at a time so the ~148 live tiles share A/B panels in L2); the
+//    kernel evaluates that layout's inverse (tile_coords below), which
+//    tests/test_gemm_raster.py derives with inv_symbolic and checks.
+//  * smem operand layouts are the UMMA canonical K-major SWIZZLE_128B atoms
+//    (8 rows x 128 B, XOR of 16-byte chunks by row % 8) that TMA produces.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+
 #include "lego_common.h"
 
-extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N,
-                                      int64_t K, int64_t batch, int32_t raster, void* stream) {
-    (void)A; (void)B; (void)C; (void)M; (void)N; (void)K; (void)batch; (void)raster; (void)stream;
-    return lego_fail(LEGO_E_UNSUPPORTED, "lego_gemm_bf16 not built yet");
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64;          // CTA tile (K step = one 128-byte swizzle row)
+constexpr int STAGES = 4;
+constexpr int UMMA_K = 16;
+constexpr int A_BYTES = BM * BK * 2;                // 16 KiB
+constexpr int B_BYTES = BN * BK * 2;                // 32 KiB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_THREADS = 192;
+constexpr int ACC_COLS = BN;                        // fp32 accumulator columns per buffer
+constexpr int TMEM_COLS = 2 * ACC_COLS;             // double buffered: 512 columns
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int GROUP_M = 16;                         // raster group (LEGO GroupBy tile)
+
+// ---- PTX wrappers ---------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}"
+        :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];"
+        :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1),
+           "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms 1024 B apart
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr & 0x3FFFF) >> 4);         // start address        [0,14)
+    d |= static_cast<uint64_t>(1) << 16;                        // LBO (unused, 1)      [16,30)
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;                // SBO = 1024 B         [32,46)
+    d |= static_cast<uint64_t>(1) << 46;                        // version = 1 (sm100)  [46,48)
+    d |= static_cast<uint64_t>(2) << 61;                        // SWIZZLE_128B         [61,64)
+    return d;
+}
+
+// instruction descriptor: kind::f16, A/B bf16 K-major, D fp32, M=128, N=256
+__host__ __device__ constexpr uint32_t make_idesc() {
+    return (1u << 4)                       // D format F32
+           | (1u << 7)                     // A format BF16
+           | (1u << 10)                    // B format BF16
+           | (uint32_t(BN >> 3) << 17)     // N >> 3
+           | (uint32_t(BM >> 4) << 24);    // M >> 4
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+
+// LEGO raster: tile t -> (batch, m-block, n-block).  The layout
+//   GroupBy([MB/G, NB, G]).OrderBy(Row(MB/G, NB, G)),  inv(t) = (g, n, m_in)
+// lists tiles group by group (G m-blocks), n-blocks inside a group,
+// m fastest; m-block = g*G + m_in.  Falls back to G = MB % G tail groups.
+struct Raster {
+    int mb, nb, per_batch;
+    __device__ __forceinline__ void coords(int t, int& b, int& m, int& n) const {
+        b = t / per_batch;
+        int r = t - b * per_batch;
+        const int full = (mb / GROUP_M) * GROUP_M;         // m-blocks in complete groups
+        const int g_tiles = GROUP_M * nb;
+        if (r < (full / GROUP_M) * g_tiles || full == mb) {
+            const int g = r / g_tiles;
+            const int rem = r - g * g_tiles;
+            n = rem / GROUP_M;
+            m = g * GROUP_M + (rem - n * GROUP_M);
+        } else {                                           // tail group of mb % G m-blocks
+            const int tail = mb - full;
+            const int rem = r - (full / GROUP_M) * g_tiles;
+            n = rem / tail;
+            m = full + (rem - n * tail);
+        }
+    }
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                  __nv_bfloat16* __restrict__ C, int M, int N, int K, int batch, int raster_mode) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    unsigned char* sA = smem;
+    unsigned char* sB = smem + STAGES * A_BYTES;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty_bar = full_bar + STAGES;
+    uint64_t* acc_full = empty_bar + STAGES;       // [2]
+    uint64_t* acc_empty = acc_full + 2;            // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int kblocks = K / BK;
+    Raster ras{M / BM, N / BN, (M / BM) * (N / BN)};
+    const int total_tiles = ras.per_batch * batch;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmap_a);
+        prefetch_tmap(&tmap_b);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&acc_full[a], 1);
+            mbar_init(&acc_empty[a], 4);            // one arrive per epilogue warp
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(tmem_slot)), "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+                int b, mb, nb;
+                if (raster_mode) ras.coords(t, b, mb, nb);
+                else { b = t / ras.per_batch; int r = t - b * ras.per_batch; mb = r / ras.nb; nb = r - mb * ras.nb; }
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                    mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
+                    tma_load_3d(sA + stage * A_BYTES, &tmap_a, &full_bar[stage], kb * BK, mb * BM, b);
+                    tma_load_3d(sB + stage * B_BYTES, &tmap_b, &full_bar[stage], kb * BK, nb * BN, b);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        constexpr uint32_t idesc = make_idesc();
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * ACC_COLS;
+            for (int kb = 0; kb < kblocks; ++kb) {
+                mbar_wait(&full_bar[stage], phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+                    const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / UMMA_K; ++k) {
+                        // advancing along K inside the 128-byte swizzle row = +32 B per UMMA_K
+                        tc_mma(d_tmem, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc,
+                               (kb | k) != 0);
+                    }
+                    tc_commit(&empty_bar[stage]);           // smem slot free once these MMAs finish
+                    if (kb == kblocks - 1) tc_commit(&acc_full[acc]);
+                }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else {
+        // ===================== epilogue (warps 2..5) =====================
+        const int quarter = warp & 3;                         // TMEM lanes 32*quarter .. +31
+        int it = 0;
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+            int b, mb, nb;
+            if (raster_mode) ras.coords(t, b, mb, nb);
+            else { b = t / ras.per_batch; int r = t - b * ras.per_batch; mb = r / ras.nb; nb = r - mb * ras.nb; }
+            const int acc = it & 1;
+            mbar_wait(&acc_full[acc], (it >> 1) & 1);
+            tc_fence_after();
+            const int row = mb * BM + quarter * 32 + lane;
+            __nv_bfloat16* crow = C + (static_cast<size_t>(b) * M + row) * static_cast<size_t>(N) + nb * BN;
+            const uint32_t taddr = tmem_base + acc * ACC_COLS + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t v[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+                      "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+                      "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr + c));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                uint4* dst = reinterpret_cast<uint4*>(crow + c);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 o;
+                    o.x = pack_bf16(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
+                    o.y = pack_bf16(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
+                    o.z = pack_bf16(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
+                    o.w = pack_bf16(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
+                    dst[q] = o;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "r"(TMEM_COLS));
+    }
+}
+
+// ---- host side ------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+lego_status make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t batch, int box_rows) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return lego_fail(LEGO_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)(rows * K * 2)};
+    cuuint32_t box[3] = {BK, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return lego_fail(LEGO_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return LEGO_OK;
+}
+
+}  // namespace
+
+extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
+                                      int64_t batch, int32_t raster, void* stream) {
+    if (M <= 0 || N <= 0 || K <= 0 || batch <= 0)
+        return lego_fail(LEGO_E_SHAPE, "gemm shape must be positive");
+    if (M % BM || N % BN || K % BK)
+        return lego_fail(LEGO_E_SHAPE, "gemm needs M %% %d == 0, N %% %d == 0, K %% %d == 0 (got %lld %lld %lld)",
+                         BM, BN, BK, (long long)M, (long long)N, (long long)K);
+    if (M * batch > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+        return lego_fail(LEGO_E_SHAPE, "gemm dimensions too large");
+    if (((uintptr_t)A | (uintptr_t)B | (uintptr_t)C) & 15)
+        return lego_fail(LEGO_E_ARG, "gemm buffers must be 16-byte aligned");
+    CUtensorMap ma, mb;
+    LEGO_TRY(make_map(&ma, A, M, K, batch, BM));
+    LEGO_TRY(make_map(&mb, B, N, K, batch, BN));
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [] {
+        attr_err = cudaFuncSetAttribute(gemm_bf16_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    });
+    LEGO_TRY(lego_cuda_check(attr_err, "cudaFuncSetAttribute(gemm smem)"));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = (M / BM) * (N / BN) * batch;
+    const int grid = (int)(tiles < sms ? tiles : sms);
+    gemm_bf16_tcgen05<<<grid, NUM_THREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
+        ma, mb, static_cast<__nv_bfloat16*>(C), (int)M, (int)N, (int)K, (int)batch, raster);
+    return lego_cuda_check(cudaGetLastError(), "gemm launch");
 }

@@ -210,3 +210,95 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
     for (int c = 0; c < LEGO_V; ++c) lego_st16(dp + (long long)c * gen::DY * LEGO_ELEM, cols[c]);
 }
 #endif
+
+// ---------------------------------------------------------------------------
+#if LEGO_KIND == 3
+// anti-diagonal band tiles.  The layout side is GroupBy([n,n]).OrderBy(GenP
+// antidiag): its positions along one anti-diagonal t = i + j are consecutive
+// in i, while row-major positions along one row are consecutive in j.  A CTA
+// owns BR rows x BK anti-diagonals: the row-major side moves BR runs of BK
+// consecutive elements (row i, columns t0-i ...), the layout side BK runs of
+// BR consecutive elements (diagonal t, rows i0 ...), both coalesced, with
+// the transpose done in padded shared memory.  gen::pos_of(x) is the
+// generated antidiag apply (reference layout.py:564-570) evaluated once per
+// run to find each diagonal run's base.  LEGO_DIR 0: row-major -> layout
+// (scatter), 1: layout -> row-major (gather).
+typedef lego_elem<LEGO_ELEM>::t lego_e;
+#define BR 64
+#define BK 64
+
+LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
+                                                   unsigned char* __restrict__ dst,
+                                                   long long src_stride, long long dst_stride) {
+    __shared__ lego_e tile[BR][BK + 1];
+    __shared__ long long run_base[BK];
+    const long long n = gen::NN;
+    const lego_e* s = reinterpret_cast<const lego_e*>(src) + (long long)blockIdx.y * src_stride;
+    lego_e* d = reinterpret_cast<lego_e*>(dst) + (long long)blockIdx.y * dst_stride;
+    const long long ri = blockIdx.x / gen::KBLOCKS;
+    const long long kk = blockIdx.x - ri * gen::KBLOCKS;
+    const long long i0 = ri * BR;
+    const long long t0 = (i0 / BK + kk) * BK;
+    if (t0 > i0 + BR - 1 + n - 1) return;             // band right of the matrix
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // base position of each diagonal's run: pos(i, t-i) = base_t + i
+    if (threadIdx.x < BK) {
+        const long long t = t0 + threadIdx.x;
+        long long iv = t - (n - 1);
+        if (iv < i0) iv = i0;
+        long long b = -1;
+        if (t <= 2 * n - 2 && iv <= t && iv < i0 + BR) {
+            long long p;
+            gen::pos_of(iv * n + (t - iv), p);
+            b = p - iv;
+        }
+        run_base[threadIdx.x] = b;
+    }
+#if LEGO_DIR == 0
+    // rows: read BK consecutive elements of row i starting at column t0 - i
+    for (int r = warp; r < BR; r += 8) {
+        const long long i = i0 + r;
+#pragma unroll
+        for (int h = 0; h < BK; h += 32) {
+            const long long j = t0 + h + lane - i;
+            if (j >= 0 && j < n) tile[r][h + lane] = s[i * n + j];
+        }
+    }
+    __syncthreads();
+    // diagonals: write BR consecutive positions base_t + i
+    for (int k = warp; k < BK; k += 8) {
+        const long long t = t0 + k;
+        const long long b = run_base[k];
+        if (b < 0) continue;
+#pragma unroll
+        for (int h = 0; h < BR; h += 32) {
+            const long long i = i0 + h + lane;
+            const long long j = t - i;
+            if (j >= 0 && j < n) d[b + i] = tile[h + lane][k];
+        }
+    }
+#else
+    __syncthreads();
+    for (int k = warp; k < BK; k += 8) {
+        const long long t = t0 + k;
+        const long long b = run_base[k];
+        if (b < 0) continue;
+#pragma unroll
+        for (int h = 0; h < BR; h += 32) {
+            const long long i = i0 + h + lane;
+            const long long j = t - i;
+            if (j >= 0 && j < n) tile[h + lane][k] = s[b + i];
+        }
+    }
+    __syncthreads();
+    for (int r = warp; r < BR; r += 8) {
+        const long long i = i0 + r;
+#pragma unroll
+        for (int h = 0; h < BK; h += 32) {
+            const long long j = t0 + h + lane - i;
+            if (j >= 0 && j < n) d[i * n + j] = tile[r][h + lane];
+        }
+    }
+#endif
+}
+#endif

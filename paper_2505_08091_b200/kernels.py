@@ -112,6 +112,9 @@ class RemapPlan:
 def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
     if elem_bytes not in (1, 2, 4, 8, 16):
         raise UnsupportedNode(f"element size {elem_bytes} not supported (1, 2, 4, 8 or 16 bytes)")
+    band = _band_plan(src_layout, dst_layout, elem_bytes)
+    if band is not None:
+        return band
     f, g, n_dst, n_src = lower.gather_expr(src_layout, dst_layout)
     lo, _hi = lower.value_range(g)
     masked = lo < 0
@@ -147,6 +150,36 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
                            "LEGO_MASKED": int(masked), "LEGO_UNROLL": unroll})
     return RemapPlan(runtime.KIND_GATHER, n_dst, n_src, elem_bytes, contig, masked, src, info,
                      f"contiguous={contig}, masked={masked}")
+
+
+BAND_ROWS, BAND_DIAGS = 64, 64
+
+
+def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
+    """Row-major <-> anti-diagonal layout: band tiles (LEGO_KIND 3)."""
+    if elem_bytes not in (1, 2, 4, 8):
+        return None
+    if src_layout is None and dst_layout is not None:
+        side, direction = dst_layout, 0
+    elif dst_layout is None and src_layout is not None:
+        side, direction = src_layout, 1
+    else:
+        return None
+    n = lower.antidiag_side(side)
+    if n is None or n % BAND_ROWS or not lower.diagonal_runs_contiguous(side, n):
+        return None
+    x = lower.flat_var("x", n * n)
+    pos = lower.simplify(lower.as_expr(lower.apply_flat(side, x)))
+    kblocks = (n + BAND_ROWS + BAND_DIAGS - 2) // BAND_DIAGS + 1
+    body = codegen.constant("NN", n) + codegen.constant("KBLOCKS", kblocks)
+    body += codegen.generate("pos_of", [x], {"p": pos}).source
+    units = (n // BAND_ROWS) * kblocks
+    info = runtime.ProgramInfo(kind=runtime.KIND_BAND, elem_bytes=elem_bytes, n=n * n, units=units,
+                               unit_threads=256, block=256, smem_bytes=0)
+    src = _assemble(body, {"LEGO_KIND": 3, "LEGO_ELEM": elem_bytes, "LEGO_DIR": direction})
+    return RemapPlan(runtime.KIND_BAND, n * n, n * n, elem_bytes, False, False, src, info,
+                     f"band {BAND_ROWS} rows x {BAND_DIAGS} diagonals, "
+                     f"{'scatter' if direction == 0 else 'gather'}")
 
 
 def _remap_program(src_layout, dst_layout, elem_bytes):

@@ -271,5 +271,33 @@ def transpose_plan(g: Expr, f: Var, n: int, elem_bytes: int) -> Optional[Transpo
     return TransposePlan(tiles, sx, y_lo, f0, s0, t, tx, ty)
 
 
+def antidiag_side(layout) -> Optional[int]:
+    """n if the layout is GroupBy([n, n]).OrderBy(GenP([n, n], antidiag))."""
+    from .layout import GenP
+    if not isinstance(layout, GroupBy) or layout.injective or len(layout.tiles) != 1:
+        return None
+    if len(layout.orders) != 1 or len(layout.orders[0].perms) != 1:
+        return None
+    p = layout.orders[0].perms[0]
+    if not isinstance(p, GenP) or p.name != "antidiag" or len(p.shape) != 2:
+        return None
+    n = p.shape[0]
+    if tuple(layout.dims) != (n, n):
+        return None
+    return n
+
+
+def diagonal_runs_contiguous(layout, n: int) -> bool:
+    """Prove pos(i+1, t-i-1) == pos(i, t-i) + 1 on every anti-diagonal t."""
+    # the layout is one GenP over its whole logical shape, so on in-range
+    # coordinates apply == the GenP's own symbolic fwd (layout.py:187-191)
+    p = layout.orders[0].perms[0]
+    i = Var("i", VarRange(0, n - 1))
+    t = Var("t", VarRange(0, 2 * n - 1))
+    a = p.fwd.symbolic((i + 1, t - i - 1))
+    b = p.fwd.symbolic((i, t - i))
+    return simplify(as_expr(a) - as_expr(b) - 1) == IntConst(0)
+
+
 def value_range(e: Expr):
     return Intervals().of(e)

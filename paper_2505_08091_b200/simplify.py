@@ -409,8 +409,27 @@ class _Normaliser:
     def finish_sum(self, lin: Lin) -> Expr:
         changed = True
         while changed and len(lin.terms) > 1:
-            changed = self.merge_digits(lin)
+            changed = self.merge_digits(lin) or self.fuse_selects(lin)
         return _build(lin)
+
+    def fuse_selects(self, lin: Lin) -> bool:
+        """c1*sel(p, a1, b1) + c2*sel(p, a2, b2) -> sel(p, c1*a1 + c2*a2, c1*b1 + c2*b2)."""
+        by_cond: Dict = {}
+        for atom in lin.terms:
+            if type(atom) is Select:
+                by_cond.setdefault(atom.cond, []).append(atom)
+        for cond, atoms in by_cond.items():
+            if len(atoms) < 2:
+                continue
+            then, orelse = Lin(), Lin()
+            for a in atoms:
+                c = lin.terms.pop(a)
+                then.add(_lin_of(a.then).scaled(c))
+                orelse.add(_lin_of(a.orelse).scaled(c))
+            fused = self.run(Select(cond, _build(then), _build(orelse)))
+            lin.add(_lin_of(fused))
+            return True
+        return False
 
     def merge_digits(self, lin: Lin) -> bool:
         """Fold two div/mod atoms over the same base into one atom.

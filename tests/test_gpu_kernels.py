@@ -1,0 +1,60 @@
+"""Fixed kernels on the GPU: tcgen05 GEMM (max-rel <= 1e-2 vs fp32/fp64),
+row softmax (<= 1e-5 vs float64), Needleman-Wunsch (bit-exact vs the C DP)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2505_08091_b200 import kernels as K  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def _gemm_check(M, N, Kd, batch=1, raster=1, seed=5):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    a = torch.randn(batch, M, Kd, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(batch, N, Kd, device="cuda", generator=g).to(torch.bfloat16)
+    c = K.gemm(a, b, raster=raster)
+    ref = torch.matmul(a.double(), b.double().transpose(-1, -2))
+    err = (c.double() - ref).abs()
+    # max-rel with the tolerance of north_star: |C - ref| / max(|ref|, 1e-2 * max|ref|)
+    denom = torch.clamp(ref.abs(), min=1e-2 * ref.abs().max().item())
+    rel = (err / denom).max().item()
+    assert rel <= 1e-2, (M, N, Kd, batch, rel)
+    return rel
+
+
+def test_gemm_small_shapes():
+    _gemm_check(128, 256, 64)
+    _gemm_check(256, 512, 128, batch=2)
+    _gemm_check(384, 256, 1024, raster=0)
+    _gemm_check(2048, 1024, 512, batch=3)
+
+
+def test_gemm_8192_cubed():
+    _gemm_check(8192, 8192, 8192)
+
+
+def test_gemm_rejects_bad_shapes():
+    import paper_2505_08091_b200 as L
+    a = torch.zeros(100, 64, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(L.ShapeMismatch):
+        K.gemm(a, a)
+
+
+@pytest.mark.parametrize("n", [1, 7, 64, 100, 257, 1024])
+def test_nw_vs_c_dp(n):
+    rng = np.random.default_rng(n)
+    sim = rng.integers(-10, 11, size=(2, n, n), dtype=np.int32)
+    got = K.nw_score(torch.from_numpy(sim).cuda(), 10).cpu().numpy()
+    for b in range(2):
+        np.testing.assert_array_equal(got[b], O.nw(sim[b], 10))
+
+
+def test_nw_16384():
+    rng = np.random.default_rng(4)
+    n = 16384
+    sim = rng.integers(-10, 11, size=(n, n), dtype=np.int32)
+    got = K.nw_score(torch.from_numpy(sim).cuda(), 10).cpu().numpy()
+    np.testing.assert_array_equal(got, O.nw(sim, 10))
