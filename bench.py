@@ -99,7 +99,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:  # noqa: BLE001
                 pass
-            self._stop.wait(0.02)
+            self._stop.wait(0.002)
 
     def __exit__(self, *exc):
         self._stop.set()
@@ -321,7 +321,7 @@ def other_kernels(args, pk, world):
     import paper_2505_08091_b200 as L
     from paper_2505_08091_b200 import kernels as K
     res = {}
-    steps, warm = max(5, args.steps), max(3, args.warmup)
+    steps, warm = max(5, min(args.steps, 50)), max(3, min(args.warmup, 5))
 
     def hbm_entry(name, nbytes, fn, traffic_key, extra=None):
         ms = time_steps(fn, steps, warm, world) / steps
@@ -355,8 +355,8 @@ def other_kernels(args, pk, world):
     try:
         sim = torch.randint(-10, 11, (16384, 16384), device="cuda", dtype=torch.int32)
         score = torch.empty(16385, 16385, device="cuda", dtype=torch.int32)
-        ms = time_steps(lambda: K.nw_score(sim, 10, out=score), max(3, steps // 2), 2, world)
-        ms /= max(3, steps // 2)
+        ms = time_steps(lambda: K.nw_score(sim, 10, out=score), 5, 3, world)
+        ms /= 5
         cells = 16384 * 16384
         res["cfg4b_nw_wavefront_i32"] = {"GCUPS": round(cells / (ms * 1e-3) / 1e9, 1),
                                          "us": round(ms * 1e3, 1),
@@ -382,8 +382,8 @@ def other_kernels(args, pk, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="lego", choices=["lego", "reference"])
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -226,77 +226,98 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
 typedef lego_elem<LEGO_ELEM>::t lego_e;
 #define BR 64
 #define BK 64
+// 32-bit index arithmetic: the planner only selects this kernel when n*n < 2^31
 
 LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
                                                    unsigned char* __restrict__ dst,
                                                    long long src_stride, long long dst_stride) {
     __shared__ lego_e tile[BR][BK + 1];
-    __shared__ long long run_base[BK];
-    const long long n = gen::NN;
+    __shared__ int run_base[BK];
+    const int n = gen::NN;
     const lego_e* s = reinterpret_cast<const lego_e*>(src) + (long long)blockIdx.y * src_stride;
     lego_e* d = reinterpret_cast<lego_e*>(dst) + (long long)blockIdx.y * dst_stride;
-    const long long ri = blockIdx.x / gen::KBLOCKS;
-    const long long kk = blockIdx.x - ri * gen::KBLOCKS;
-    const long long i0 = ri * BR;
-    const long long t0 = (i0 / BK + kk) * BK;
+    const int ri = blockIdx.x / gen::KBLOCKS;
+    const int kk = blockIdx.x - ri * gen::KBLOCKS;
+    const int i0 = ri * BR;
+    const int t0 = (i0 / BK + kk) * BK;
     if (t0 > i0 + BR - 1 + n - 1) return;             // band right of the matrix
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // base position of each diagonal's run: pos(i, t-i) = base_t + i
     if (threadIdx.x < BK) {
-        const long long t = t0 + threadIdx.x;
-        long long iv = t - (n - 1);
-        if (iv < i0) iv = i0;
-        long long b = -1;
+        const int t = t0 + threadIdx.x;
+        int iv = max(t - (n - 1), i0);
+        int b = -1;
         if (t <= 2 * n - 2 && iv <= t && iv < i0 + BR) {
             long long p;
-            gen::pos_of(iv * n + (t - iv), p);
-            b = p - iv;
+            gen::pos_of((long long)iv * n + (t - iv), p);
+            b = (int)p - iv;
         }
         run_base[threadIdx.x] = b;
     }
+    constexpr int RPW = BR / 8;                        // rows (or diagonals) per warp
 #if LEGO_DIR == 0
-    // rows: read BK consecutive elements of row i starting at column t0 - i
-    for (int r = warp; r < BR; r += 8) {
-        const long long i = i0 + r;
+    {   // rows: BK consecutive elements of row i from column t0 - i; all loads first
+        lego_e v[RPW][BK / 32];
 #pragma unroll
-        for (int h = 0; h < BK; h += 32) {
-            const long long j = t0 + h + lane - i;
-            if (j >= 0 && j < n) tile[r][h + lane] = s[i * n + j];
+        for (int q = 0; q < RPW; ++q) {
+            const int i = i0 + warp + 8 * q;
+            const int j0 = t0 - i;
+            const lego_e* row = s + i * n;
+#pragma unroll
+            for (int h = 0; h < BK / 32; ++h) {
+                const int j = j0 + 32 * h + lane;
+                v[q][h] = ((unsigned)j < (unsigned)n) ? __ldg(row + j) : (lego_e)0;
+            }
         }
+#pragma unroll
+        for (int q = 0; q < RPW; ++q)
+#pragma unroll
+            for (int h = 0; h < BK / 32; ++h) tile[warp + 8 * q][32 * h + lane] = v[q][h];
     }
     __syncthreads();
-    // diagonals: write BR consecutive positions base_t + i
-    for (int k = warp; k < BK; k += 8) {
-        const long long t = t0 + k;
-        const long long b = run_base[k];
+    // diagonals: BR consecutive positions base_t + i
+#pragma unroll
+    for (int q = 0; q < BK / 8; ++q) {
+        const int k = warp + 8 * q;
+        const int t = t0 + k;
+        const int b = run_base[k];
         if (b < 0) continue;
 #pragma unroll
-        for (int h = 0; h < BR; h += 32) {
-            const long long i = i0 + h + lane;
-            const long long j = t - i;
-            if (j >= 0 && j < n) d[b + i] = tile[h + lane][k];
+        for (int h = 0; h < BR / 32; ++h) {
+            const int i = i0 + 32 * h + lane;
+            if ((unsigned)(t - i) < (unsigned)n) d[b + i] = tile[32 * h + lane][k];
         }
     }
 #else
     __syncthreads();
-    for (int k = warp; k < BK; k += 8) {
-        const long long t = t0 + k;
-        const long long b = run_base[k];
-        if (b < 0) continue;
+    {
+        lego_e v[BK / 8][BR / 32];
 #pragma unroll
-        for (int h = 0; h < BR; h += 32) {
-            const long long i = i0 + h + lane;
-            const long long j = t - i;
-            if (j >= 0 && j < n) tile[h + lane][k] = s[b + i];
+        for (int q = 0; q < BK / 8; ++q) {
+            const int k = warp + 8 * q;
+            const int t = t0 + k;
+            const int b = run_base[k];
+#pragma unroll
+            for (int h = 0; h < BR / 32; ++h) {
+                const int i = i0 + 32 * h + lane;
+                v[q][h] = (b >= 0 && (unsigned)(t - i) < (unsigned)n) ? __ldg(s + b + i) : (lego_e)0;
+            }
         }
+#pragma unroll
+        for (int q = 0; q < BK / 8; ++q)
+#pragma unroll
+            for (int h = 0; h < BR / 32; ++h) tile[32 * h + lane][warp + 8 * q] = v[q][h];
     }
     __syncthreads();
-    for (int r = warp; r < BR; r += 8) {
-        const long long i = i0 + r;
 #pragma unroll
-        for (int h = 0; h < BK; h += 32) {
-            const long long j = t0 + h + lane - i;
-            if (j >= 0 && j < n) d[i * n + j] = tile[r][h + lane];
+    for (int q = 0; q < RPW; ++q) {
+        const int i = i0 + warp + 8 * q;
+        const int j0 = t0 - i;
+        lego_e* row = d + i * n;
+#pragma unroll
+        for (int h = 0; h < BK / 32; ++h) {
+            const int j = j0 + 32 * h + lane;
+            if ((unsigned)j < (unsigned)n) row[j] = tile[warp + 8 * q][32 * h + lane];
         }
     }
 #endif

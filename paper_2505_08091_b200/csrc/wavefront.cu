@@ -4,21 +4,22 @@
 //   S[0][j] = -j*p,  S[i][0] = -i*p,
 //   S[i][j] = max(S[i-1][j-1] + sim[i-1][j-1], S[i-1][j] - p, S[i][j-1] - p)
 //
-// Decomposition (B200-first, no host loop over diagonals): the n columns are
-// cut into 32-wide strips, one warp per strip, claimed in order from an
-// atomic ticket so a strip's left neighbour is always already running (no
-// deadlock, no grid sync).  Inside a strip the warp sweeps the strip's cells
-// in anti-diagonal order: lane j owns column j and at step s computes row
-// s - j, so each step is one anti-diagonal of the 32-wide strip (the LEGO
-// antidiag order of the paper's NW kernel).  The left
-// neighbour's value arrives by warp shuffle, the up value is the lane's own
-// previous result, the diagonal value is the previous shuffle.  sim rows are
-// staged 32x32 through shared memory with coalesced loads (prefetched one
-// block ahead) and read back along the anti-diagonal -- bank = lane, no
-// conflicts; results go through a second 32x32 tile and leave as coalesced
-// row segments.  Strips hand their last column to the right neighbour
-// through a global boundary array published every 32 rows with st.release /
-// ld.acquire.
+// Decomposition (no host loop over diagonals, no grid sync):
+//  * the n columns are cut into 128-wide strips, one warp per strip, claimed
+//    in order from an atomic ticket, so a strip's left neighbour is always
+//    already running;
+//  * inside a strip the warp sweeps anti-diagonally: lane j owns columns
+//    4j..4j+3 and at step s computes row s - j, i.e. every step is one
+//    anti-diagonal of the (rows x 32 lane-columns) grid -- the LEGO antidiag
+//    order of the paper's NW kernel.  The value from the
+//    left arrives by warp shuffle, the up and diagonal values are the lane's
+//    own previous row, so one step costs one shuffle plus a 4-cell chain;
+//  * sim is staged 32 rows x 128 columns at a time in shared memory by
+//    cp.async (issued one block ahead, triple buffered), read back along the
+//    anti-diagonal with conflict-free 16-byte loads; results go through a
+//    second tile and leave as coalesced row segments;
+//  * strips hand their last column to the right neighbour through a global
+//    boundary array published every 32 rows with st.release / ld.acquire.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -27,8 +28,13 @@
 
 namespace {
 
-constexpr int WARPS = 8;
-constexpr int TILE = 32;
+constexpr int TILE = 32;                 // rows per staged block
+constexpr int CPL = 4;                   // columns per lane
+constexpr int STRIP = 32 * CPL;          // columns per warp strip
+constexpr int SIM_BUFS = 3;
+constexpr int OUT_BUFS = 2;
+constexpr int BLOCK_ELEMS = TILE * STRIP;
+constexpr int SMEM_BYTES = (SIM_BUFS + OUT_BUFS) * BLOCK_ELEMS * 4 + 2 * TILE * 4;
 
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
@@ -38,6 +44,16 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                 :: "r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;"
+                 :: "r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long long batch) {
     const long long w = n + 1;
@@ -51,16 +67,39 @@ __global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long
     }
 }
 
-__global__ void __launch_bounds__(WARPS * 32)
+// stage sim rows [32k, 32k+32) of the strip into buf (cp.async, no wait)
+__device__ __forceinline__ void stage_sim(int32_t* buf, const int32_t* simb, int n, int k, int col0, int lane,
+                                          bool vec_ok) {
+    for (int r = 0; r < TILE; ++r) {
+        const int row = k * TILE + r;
+        if (row >= n) break;
+        const int32_t* src = simb + (long long)row * n + col0;
+        int32_t* dst = buf + r * STRIP;
+        if (vec_ok) {
+            if (col0 + CPL * lane < n) cp_async16(dst + CPL * lane, src + CPL * lane);
+        } else {
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int c = q * 32 + lane;
+                if (col0 + c < n) cp_async4(dst + c, src + c);
+            }
+        }
+    }
+    cp_async_commit();
+}
+
+__global__ void __launch_bounds__(32)
 nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, int p, int strips_per_matrix,
           int total_strips, int* __restrict__ ticket, int* __restrict__ progress, int32_t* __restrict__ bnd) {
-    extern __shared__ int32_t smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int32_t* s_sim = smem + warp * (4 * TILE * TILE);      // [2][32][32]
-    int32_t* s_out = s_sim + 2 * TILE * TILE;              // [2][32][32]
+    extern __shared__ __align__(16) int32_t smem[];
+    int32_t* s_sim = smem;                                   // [3][32][128]
+    int32_t* s_out = s_sim + SIM_BUFS * BLOCK_ELEMS;         // [2][32][128]
+    int32_t* s_bnd = s_out + OUT_BUFS * BLOCK_ELEMS;         // [2][32]
+    const int lane = threadIdx.x;
     const long long ld = (long long)n + 1;
     const int n_pad = (n + TILE - 1) / TILE * TILE;
     const int nblocks = n_pad / TILE;
+    const bool vec_ok = (n % 4) == 0;
 
     for (;;) {
         int strip = 0;
@@ -72,80 +111,91 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
         const int32_t* simb = sim + (long long)b * n * n;
         int32_t* sc = score + (long long)b * ld * ld;
         int32_t* my_bnd = bnd + (long long)strip * n_pad;
-        const int32_t* left_bnd = my_bnd - n_pad;          // strip - 1 (same matrix when w > 0)
+        const int32_t* left_bnd = my_bnd - n_pad;
         int* my_prog = progress + strip;
         const int* left_prog = progress + strip - 1;
-        const int col = w * TILE + lane;                  // 0-based sim column; DP column col + 1
-        const bool col_ok = col < n;
+        const int col0 = w * STRIP;
+        const int c_lane = col0 + CPL * lane;                 // first 0-based sim column of this lane
 
-        // prefetch sim block 0 (rows 0..31 of this strip), coalesced per row
-        int32_t pre[TILE];
+        stage_sim(s_sim, simb, n, 0, col0, lane, vec_ok);
+
+        int32_t h[CPL];
 #pragma unroll
-        for (int r = 0; r < TILE; ++r) pre[r] = (r < n && col_ok) ? __ldg(simb + (long long)r * n + col) : 0;
-
-        int32_t h = -(col + 1) * p;                        // S[0][col+1] until the lane starts
-        int32_t left_prev = -col * p;                      // S[0][col]
-        int known = 0;                                     // rows published by the left strip
-        int32_t lane0_diag = -(w * TILE) * p;              // S[i][w*32] for lane 0
+        for (int k = 0; k < CPL; ++k) h[k] = -(c_lane + k + 1) * p;   // S[0][c+1]
+        int32_t left_prev = -c_lane * p;                               // S[0][c_lane]
 
         for (int s = 0; s < n_pad + TILE - 1; ++s) {
+            const int blk = s / TILE;
             if ((s & (TILE - 1)) == 0) {
-                const int k = s / TILE;
-                if (k < nblocks) {
-                    int32_t* dst = s_sim + (k & 1) * TILE * TILE;
-#pragma unroll
-                    for (int r = 0; r < TILE; ++r) dst[r * TILE + lane] = pre[r];
-                    const int nk = k + 1;
-                    if (nk < nblocks) {
-#pragma unroll
-                        for (int r = 0; r < TILE; ++r) {
-                            const int row = nk * TILE + r;
-                            pre[r] = (row < n && col_ok) ? __ldg(simb + (long long)row * n + col) : 0;
+                if (blk < nblocks) {
+                    // left boundary rows [s, s+32) for lane 0, once the left strip published them
+                    if (w > 0) {
+                        const int need = min(s + TILE, n);
+                        if (lane == 0) {
+                            while (ld_acquire(left_prog) < need) {
+                            }
                         }
+                        __syncwarp();
+                        if (s + lane < n) s_bnd[(blk & 1) * TILE + lane] = __ldcg(left_bnd + s + lane);
+                    }
+                    // blocks blk-1 (lanes still finishing it) and blk are live; stage blk+1
+                    // into the third buffer, whose block blk-2 retired at step 32*blk - 2
+                    if (blk + 1 < nblocks) {
+                        stage_sim(s_sim + ((blk + 1) % SIM_BUFS) * BLOCK_ELEMS, simb, n, blk + 1, col0, lane,
+                                  vec_ok);
+                        asm volatile("cp.async.wait_group 1;" ::: "memory");   // block blk landed
+                    } else {
+                        cp_async_wait_all();
                     }
                 }
                 __syncwarp();
             }
-            const int i = s - lane;                        // 0-based row of this lane at step s
-            int32_t from_left = __shfl_up_sync(0xffffffffu, h, 1);   // S[i+1][col] from lane-1
-            if (lane == 0) {
-                if (w == 0) {
-                    from_left = -(i + 1) * p;
-                } else if (i < n) {
-                    if (i >= known) {
-                        do { known = ld_acquire(left_prog); } while (known <= i);
-                    }
-                    from_left = __ldcg(left_bnd + i);
+            const int i = s - lane;
+            int32_t left = __shfl_up_sync(0xffffffffu, h[CPL - 1], 1);   // S[i+1][c_lane] from lane-1
+            if (lane == 0) left = w == 0 ? -(i + 1) * p : s_bnd[(blk & 1) * TILE + (s & (TILE - 1))];
+            if (i >= 0 && i < n) {
+                const int4 sv = *reinterpret_cast<const int4*>(
+                    s_sim + ((i / TILE) % SIM_BUFS) * BLOCK_ELEMS + (i & (TILE - 1)) * STRIP + CPL * lane);
+                const int32_t svals[CPL] = {sv.x, sv.y, sv.z, sv.w};
+                int32_t nh[CPL];
+                int32_t diag = left_prev, lf = left;
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                    const int32_t v = max(diag + svals[k], max(h[k], lf) - p);
+                    diag = h[k];
+                    nh[k] = v;
+                    lf = v;
                 }
-            }
-            const bool active = i >= 0 && i < n;
-            if (active) {
-                const int32_t sv = s_sim[((i / TILE) & 1) * TILE * TILE + (i & (TILE - 1)) * TILE + lane];
-                const int32_t diag = lane == 0 ? lane0_diag : left_prev;
-                const int32_t up = h;
-                int32_t v = diag + sv;
-                const int32_t g = max(up, from_left) - p;
-                h = max(v, g);
-                s_out[((i / TILE) & 1) * TILE * TILE + (i & (TILE - 1)) * TILE + lane] = h;
-                if (lane == TILE - 1) {
-                    my_bnd[i] = h;
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) h[k] = nh[k];
+                *reinterpret_cast<int4*>(s_out + ((i / TILE) & 1) * BLOCK_ELEMS + (i & (TILE - 1)) * STRIP +
+                                         CPL * lane) = make_int4(nh[0], nh[1], nh[2], nh[3]);
+                if (lane == 31) {
+                    my_bnd[i] = nh[CPL - 1];
                     if ((i & (TILE - 1)) == TILE - 1 || i == n - 1) st_release(my_prog, i + 1);
                 }
             }
-            if (lane == 0) lane0_diag = from_left;
-            left_prev = from_left;
-            // block k completes at step 32k + 62: flush its 32 rows as coalesced segments
+            left_prev = left;
+            // block k completes at step 32k + 62: flush its rows as coalesced segments
             if ((s & (TILE - 1)) == TILE - 2 && s >= 2 * TILE - 2) {
                 const int k = (s - (2 * TILE - 2)) / TILE;
                 __syncwarp();
-                const int32_t* src = s_out + (k & 1) * TILE * TILE;
+                const int32_t* src = s_out + (k & 1) * BLOCK_ELEMS;
                 for (int r = 0; r < TILE; ++r) {
                     const int row = k * TILE + r;
-                    if (row < n && col_ok) sc[(long long)(row + 1) * ld + col + 1] = src[r * TILE + lane];
+                    if (row >= n) break;
+                    int32_t* dst = sc + (long long)(row + 1) * ld + col0 + 1;
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) {
+                        const int c = q * 32 + lane;
+                        if (col0 + c < n) dst[c] = src[r * STRIP + c];
+                    }
                 }
                 __syncwarp();
             }
         }
+        cp_async_wait_all();
+        __syncwarp();
     }
 }
 
@@ -157,34 +207,35 @@ extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n
     if (batch == 0) return LEGO_OK;
     if (n > (1 << 20)) return lego_fail(LEGO_E_SHAPE, "NW n above 2^20");
     if (!sim || !score) return lego_fail(LEGO_E_ARG, "null buffer");
+    if ((uintptr_t)sim & 15) return lego_fail(LEGO_E_ARG, "sim must be 16-byte aligned");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const long long w = n + 1;
-    nw_borders<<<(unsigned)((batch * w + 255) / 256 < 4096 ? (batch * w + 255) / 256 : 4096), 256, 0, st>>>(
-        score, n, penalty, batch);
+    const long long bgrid = (batch * w + 255) / 256;
+    nw_borders<<<(unsigned)(bgrid < 4096 ? bgrid : 4096), 256, 0, st>>>(score, n, penalty, batch);
     if (n == 0) return lego_cuda_check(cudaGetLastError(), "nw borders");
-    const int strips = (int)((n + TILE - 1) / TILE);
+    const int strips = (int)((n + STRIP - 1) / STRIP);
     const long long total = (long long)strips * batch;
     if (total > INT32_MAX) return lego_fail(LEGO_E_SHAPE, "NW batch too large");
-    const int n_pad = strips * TILE;
-    // scratch: ticket + per-strip progress + boundary columns
+    const int n_pad = (int)((n + TILE - 1) / TILE * TILE);
     const size_t prog_bytes = sizeof(int) * (size_t)(total + 1);
+    const size_t bnd_off = (prog_bytes + 255) / 256 * 256;
     const size_t bnd_bytes = sizeof(int32_t) * (size_t)total * n_pad;
     char* scratch = nullptr;
-    LEGO_TRY(lego_cuda_check(cudaMallocAsync((void**)&scratch, prog_bytes + bnd_bytes, st), "cudaMallocAsync"));
+    LEGO_TRY(lego_cuda_check(cudaMallocAsync((void**)&scratch, bnd_off + bnd_bytes, st), "cudaMallocAsync"));
     LEGO_TRY(lego_cuda_check(cudaMemsetAsync(scratch, 0, prog_bytes, st), "cudaMemsetAsync"));
     int* ticket = reinterpret_cast<int*>(scratch);
     int* progress = ticket + 1;
-    int32_t* bnd = reinterpret_cast<int32_t*>(scratch + prog_bytes);
-    const int smem = WARPS * 4 * TILE * TILE * (int)sizeof(int32_t);
-    static cudaError_t attr = cudaFuncSetAttribute(nw_strips, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int32_t* bnd = reinterpret_cast<int32_t*>(scratch + bnd_off);
+    static cudaError_t attr = cudaFuncSetAttribute(nw_strips, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   SMEM_BYTES);
     LEGO_TRY(lego_cuda_check(attr, "cudaFuncSetAttribute(nw)"));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    long long ctas = (total + WARPS - 1) / WARPS;
-    if (ctas > 2LL * sms) ctas = 2LL * sms;
-    nw_strips<<<(unsigned)ctas, WARPS * 32, smem, st>>>(sim, score, (int)n, penalty, strips, (int)total, ticket,
-                                                        progress, bnd);
+    const long long cap = 2LL * sms;       // two strips per SM fit the 80 KiB of staging each
+    const long long ctas = total < cap ? total : cap;
+    nw_strips<<<(unsigned)ctas, 32, SMEM_BYTES, st>>>(sim, score, (int)n, penalty, strips, (int)total, ticket,
+                                                      progress, bnd);
     lego_status s = lego_cuda_check(cudaGetLastError(), "nw launch");
     cudaFreeAsync(scratch, st);
     return s;

@@ -166,7 +166,7 @@ def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
     else:
         return None
     n = lower.antidiag_side(side)
-    if n is None or n % BAND_ROWS or not lower.diagonal_runs_contiguous(side, n):
+    if n is None or n % BAND_ROWS or n * n >= 2 ** 31 or not lower.diagonal_runs_contiguous(side, n):
         return None
     x = lower.flat_var("x", n * n)
     pos = lower.simplify(lower.as_expr(lower.apply_flat(side, x)))
