@@ -189,6 +189,56 @@ static __device__ __forceinline__ void lego_transpose(const lego_v16 (&in)[LEGO_
 #endif
 }
 
+#if LEGO_SMEM
+// Variant with 128-byte segments on BOTH sides: a warp owns an (8V) x (8V)
+// tile; lane (xg, c) = (lane / 8, lane % 8) loads two VxV blocks (x rows
+// xg*V.. and (xg+4)*V..) along y chunk c, transposes them in registers and
+// parks the x-vectors in shared memory as [y][x-chunk] 16-byte cells whose
+// chunk index is XOR-swizzled by (y / V) % 8 (conflict-free both ways); the
+// warp then writes 4 dst rows of 8 chunks (128 B each) per instruction.
+LEGO_GLOBAL void __launch_bounds__(128) lego_remap(const unsigned char* __restrict__ src,
+                                                   unsigned char* __restrict__ dst,
+                                                   long long src_stride, long long dst_stride) {
+    extern __shared__ lego_v16 lego_cells[];               // [warp][y][swizzled x-chunk]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    lego_v16 (*cells)[8] = reinterpret_cast<lego_v16 (*)[8]>(lego_cells + warp * (8 * LEGO_V) * 8);
+    const long long t = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (t >= gen::TILES) return;
+    const unsigned char* s = src + (long long)blockIdx.y * src_stride * LEGO_ELEM;
+    unsigned char* d = dst + (long long)blockIdx.y * dst_stride * LEGO_ELEM;
+    long long f0, s0;
+    gen::origin(t, f0, s0);
+    const int c = lane & 7, xg = lane >> 3;
+    lego_v16 rows[2][LEGO_V];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const unsigned char* sp =
+            s + (s0 + (long long)((xg + 4 * h) * LEGO_V) * gen::SX + c * LEGO_V) * LEGO_ELEM;
+#pragma unroll
+        for (int r = 0; r < LEGO_V; ++r) rows[h][r] = lego_ld16(sp + (long long)r * gen::SX * LEGO_ELEM);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        lego_v16 cols[LEGO_V];
+        lego_transpose(rows[h], cols);
+        const int xc = xg + 4 * h;                          // x-chunk of these vectors
+#pragma unroll
+        for (int m = 0; m < LEGO_V; ++m) {
+            const int y = c * LEGO_V + m;
+            cells[y][xc ^ (c & 7)] = cols[m];
+        }
+    }
+    __syncwarp();
+    // store: lanes 8q..8q+7 write dst row y (8 chunks = 128 bytes)
+    const int k = lane & 7;
+#pragma unroll
+    for (int it = 0; it < 2 * LEGO_V; ++it) {
+        const int y = it * 4 + (lane >> 3);
+        const lego_v16 v = cells[y][k ^ ((y / LEGO_V) & 7)];
+        lego_st16(d + (f0 + (long long)y * gen::DY + k * LEGO_V) * LEGO_ELEM, v);
+    }
+}
+#else
 LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
                                                    unsigned char* __restrict__ dst,
                                                    long long src_stride, long long dst_stride) {
@@ -209,6 +259,7 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
 #pragma unroll
     for (int c = 0; c < LEGO_V; ++c) lego_st16(dp + (long long)c * gen::DY * LEGO_ELEM, cols[c]);
 }
+#endif  // LEGO_SMEM
 #endif
 
 // ---------------------------------------------------------------------------

@@ -13,13 +13,16 @@
 //    anti-diagonal of the (rows x 32 lane-columns) grid -- the LEGO antidiag
 //    order of the paper's NW kernel.  The value from the
 //    left arrives by warp shuffle, the up and diagonal values are the lane's
-//    own previous row, so one step costs one shuffle plus a 4-cell chain;
-//  * sim is staged 32 rows x 128 columns at a time in shared memory by
-//    cp.async (issued one block ahead, triple buffered), read back along the
-//    anti-diagonal with conflict-free 16-byte loads; results go through a
-//    second tile and leave as coalesced row segments;
-//  * strips hand their last column to the right neighbour through a global
-//    boundary array published every 32 rows with st.release / ld.acquire.
+//    own previous row: the per-step critical path is one shuffle plus a
+//    4-cell max/add chain.  Everything else is off that path:
+//  * sim is staged 32 rows x 128 columns at a time by cp.async two blocks
+//    ahead (4 buffers) and each lane's next 16-byte sim vector is read from
+//    shared memory one step early;
+//  * results go through a 32 x 128 tile and leave as coalesced row segments
+//    once a block of 32 rows is complete; at that point the strip's last
+//    column for those rows is copied to a global boundary array and
+//    published with one st.release, which the right neighbour polls with
+//    ld.acquire once per 32 rows.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -31,10 +34,11 @@ namespace {
 constexpr int TILE = 32;                 // rows per staged block
 constexpr int CPL = 4;                   // columns per lane
 constexpr int STRIP = 32 * CPL;          // columns per warp strip
-constexpr int SIM_BUFS = 3;
+constexpr int SIM_BUFS = 4;
 constexpr int OUT_BUFS = 2;
 constexpr int BLOCK_ELEMS = TILE * STRIP;
-constexpr int SMEM_BYTES = (SIM_BUFS + OUT_BUFS) * BLOCK_ELEMS * 4 + 2 * TILE * 4;
+constexpr int BND_RING = 64;
+constexpr int SMEM_BYTES = (SIM_BUFS + OUT_BUFS) * BLOCK_ELEMS * 4 + BND_RING * 4;
 
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
@@ -54,6 +58,7 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 __global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long long batch) {
     const long long w = n + 1;
@@ -67,7 +72,7 @@ __global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long
     }
 }
 
-// stage sim rows [32k, 32k+32) of the strip into buf (cp.async, no wait)
+// stage sim rows [32k, 32k+32) of the strip into buf (one cp.async group; empty past the end)
 __device__ __forceinline__ void stage_sim(int32_t* buf, const int32_t* simb, int n, int k, int col0, int lane,
                                           bool vec_ok) {
     for (int r = 0; r < TILE; ++r) {
@@ -92,9 +97,9 @@ __global__ void __launch_bounds__(32)
 nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, int p, int strips_per_matrix,
           int total_strips, int* __restrict__ ticket, int* __restrict__ progress, int32_t* __restrict__ bnd) {
     extern __shared__ __align__(16) int32_t smem[];
-    int32_t* s_sim = smem;                                   // [3][32][128]
+    int32_t* s_sim = smem;                                   // [4][32][128]
     int32_t* s_out = s_sim + SIM_BUFS * BLOCK_ELEMS;         // [2][32][128]
-    int32_t* s_bnd = s_out + OUT_BUFS * BLOCK_ELEMS;         // [2][32]
+    int32_t* s_bnd = s_out + OUT_BUFS * BLOCK_ELEMS;         // ring of 64 rows
     const int lane = threadIdx.x;
     const long long ld = (long long)n + 1;
     const int n_pad = (n + TILE - 1) / TILE * TILE;
@@ -117,66 +122,57 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
         const int col0 = w * STRIP;
         const int c_lane = col0 + CPL * lane;                 // first 0-based sim column of this lane
 
+        // block boundary event for block k: its sim landed, block k+1 in flight,
+        // left boundary rows of block k in the ring
+        auto enter_block = [&](int k) {
+            if (k + 1 < nblocks) {
+                stage_sim(s_sim + ((k + 1) & (SIM_BUFS - 1)) * BLOCK_ELEMS, simb, n, k + 1, col0, lane, vec_ok);
+                cp_async_wait_1();
+            } else {
+                cp_async_wait_all();
+            }
+            if (w > 0) {
+                const int need = min((k + 1) * TILE, n);
+                if (lane == 0) {
+                    while (ld_acquire(left_prog) < need) {
+                    }
+                }
+                __syncwarp();
+                const int row = k * TILE + lane;
+                if (row < n) s_bnd[row & (BND_RING - 1)] = __ldcg(left_bnd + row);
+            }
+            __syncwarp();
+        };
+
         stage_sim(s_sim, simb, n, 0, col0, lane, vec_ok);
+        enter_block(0);
 
         int32_t h[CPL];
 #pragma unroll
         for (int k = 0; k < CPL; ++k) h[k] = -(c_lane + k + 1) * p;   // S[0][c+1]
         int32_t left_prev = -c_lane * p;                               // S[0][c_lane]
+        int4 sv = make_int4(0, 0, 0, 0);
+        if (lane == 0) sv = *reinterpret_cast<const int4*>(s_sim);    // row 0 for lane 0
 
         for (int s = 0; s < n_pad + TILE - 1; ++s) {
-            const int blk = s / TILE;
-            if ((s & (TILE - 1)) == 0) {
-                if (blk < nblocks) {
-                    // left boundary rows [s, s+32) for lane 0, once the left strip published them
-                    if (w > 0) {
-                        const int need = min(s + TILE, n);
-                        if (lane == 0) {
-                            while (ld_acquire(left_prog) < need) {
-                            }
-                        }
-                        __syncwarp();
-                        if (s + lane < n) s_bnd[(blk & 1) * TILE + lane] = __ldcg(left_bnd + s + lane);
-                    }
-                    // blocks blk-1 (lanes still finishing it) and blk are live; stage blk+1
-                    // into the third buffer, whose block blk-2 retired at step 32*blk - 2
-                    if (blk + 1 < nblocks) {
-                        stage_sim(s_sim + ((blk + 1) % SIM_BUFS) * BLOCK_ELEMS, simb, n, blk + 1, col0, lane,
-                                  vec_ok);
-                        asm volatile("cp.async.wait_group 1;" ::: "memory");   // block blk landed
-                    } else {
-                        cp_async_wait_all();
-                    }
-                }
-                __syncwarp();
-            }
             const int i = s - lane;
             int32_t left = __shfl_up_sync(0xffffffffu, h[CPL - 1], 1);   // S[i+1][c_lane] from lane-1
-            if (lane == 0) left = w == 0 ? -(i + 1) * p : s_bnd[(blk & 1) * TILE + (s & (TILE - 1))];
+            if (lane == 0) left = w == 0 ? -(i + 1) * p : s_bnd[i & (BND_RING - 1)];
             if (i >= 0 && i < n) {
-                const int4 sv = *reinterpret_cast<const int4*>(
-                    s_sim + ((i / TILE) % SIM_BUFS) * BLOCK_ELEMS + (i & (TILE - 1)) * STRIP + CPL * lane);
                 const int32_t svals[CPL] = {sv.x, sv.y, sv.z, sv.w};
-                int32_t nh[CPL];
                 int32_t diag = left_prev, lf = left;
 #pragma unroll
                 for (int k = 0; k < CPL; ++k) {
                     const int32_t v = max(diag + svals[k], max(h[k], lf) - p);
                     diag = h[k];
-                    nh[k] = v;
+                    h[k] = v;
                     lf = v;
                 }
-#pragma unroll
-                for (int k = 0; k < CPL; ++k) h[k] = nh[k];
-                *reinterpret_cast<int4*>(s_out + ((i / TILE) & 1) * BLOCK_ELEMS + (i & (TILE - 1)) * STRIP +
-                                         CPL * lane) = make_int4(nh[0], nh[1], nh[2], nh[3]);
-                if (lane == 31) {
-                    my_bnd[i] = nh[CPL - 1];
-                    if ((i & (TILE - 1)) == TILE - 1 || i == n - 1) st_release(my_prog, i + 1);
-                }
+                *reinterpret_cast<int4*>(s_out + ((i >> 5) & 1) * BLOCK_ELEMS + (i & (TILE - 1)) * STRIP +
+                                         CPL * lane) = make_int4(h[0], h[1], h[2], h[3]);
             }
             left_prev = left;
-            // block k completes at step 32k + 62: flush its rows as coalesced segments
+            // block k completes at step 32k + 62: flush its rows, publish the boundary column
             if ((s & (TILE - 1)) == TILE - 2 && s >= 2 * TILE - 2) {
                 const int k = (s - (2 * TILE - 2)) / TILE;
                 __syncwarp();
@@ -191,8 +187,17 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                         if (col0 + c < n) dst[c] = src[r * STRIP + c];
                     }
                 }
+                const int brow = k * TILE + lane;
+                if (brow < n) my_bnd[brow] = src[lane * STRIP + STRIP - 1];
                 __syncwarp();
+                if (lane == 0) st_release(my_prog, min((k + 1) * TILE, n));
             }
+            // next step reads row i + 1; a new block enters when lane 0 crosses into it
+            if (((s + 1) & (TILE - 1)) == 0 && (s + 1) < n_pad) enter_block((s + 1) / TILE);
+            const int ni = i + 1;
+            if (ni >= 0 && ni < n)
+                sv = *reinterpret_cast<const int4*>(s_sim + ((ni >> 5) & (SIM_BUFS - 1)) * BLOCK_ELEMS +
+                                                    (ni & (TILE - 1)) * STRIP + CPL * lane);
         }
         cp_async_wait_all();
         __syncwarp();
@@ -232,7 +237,7 @@ extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long cap = 2LL * sms;       // two strips per SM fit the 80 KiB of staging each
+    const long long cap = 2LL * sms;       // two strips per SM fit the staging buffers
     const long long ctas = total < cap ? total : cap;
     nw_strips<<<(unsigned)ctas, 32, SMEM_BYTES, st>>>(sim, score, (int)n, penalty, strips, (int)total, ticket,
                                                       progress, bnd);

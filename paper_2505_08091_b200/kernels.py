@@ -123,19 +123,24 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
         raise UnsupportedNode(f"destination size {n_dst} is not a multiple of {vec} elements "
                               f"({elem_bytes}-byte elements, 16-byte vectors)")
     if not masked:
-        tp = lower.transpose_plan(g, f, n_dst, elem_bytes)
+        smem_variant = TRANSPOSE_VARIANT == "smem"
+        tp = lower.transpose_plan(g, f, n_dst, elem_bytes, 8 if smem_variant else 4, 8)
         if tp is not None:
             body = codegen.constant("N", n_dst) + codegen.constant("TILES", tp.tiles)
             body += codegen.constant("SX", tp.sx) + codegen.constant("DY", tp.dy)
             body += codegen.generate("origin", [tp.t], {"f0": tp.origin_f0,
                                                         "s0": tp.origin_s0}).source
-            warps = 8
+            warps = 4 if smem_variant else 8
+            v = 16 // elem_bytes
+            smem = warps * 8 * v * 8 * 16 if smem_variant else 0
             info = runtime.ProgramInfo(kind=runtime.KIND_TRANSPOSE, elem_bytes=elem_bytes, n=n_dst,
                                        units=(tp.tiles + warps - 1) // warps, unit_threads=32,
-                                       block=32 * warps, smem_bytes=0)
-            src = _assemble(body, {"LEGO_KIND": 2, "LEGO_ELEM": elem_bytes})
+                                       block=32 * warps, smem_bytes=smem)
+            src = _assemble(body, {"LEGO_KIND": 2, "LEGO_ELEM": elem_bytes,
+                                   "LEGO_SMEM": int(smem_variant)})
             return RemapPlan(runtime.KIND_TRANSPOSE, n_dst, n_src, elem_bytes, False, False, src,
-                             info, f"tile {tp.tx}x{tp.ty}, SX={tp.sx}, DY={tp.dy}")
+                             info, f"tile {tp.tx}x{tp.ty}{' smem' if smem_variant else ''}, "
+                                   f"SX={tp.sx}, DY={tp.dy}")
     width = 1 if masked else lower.contiguous_width(g, f, n_dst, widths=(vec,))
     contig = width >= vec
     body = codegen.constant("N", n_dst)
@@ -153,6 +158,9 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
 
 
 BAND_ROWS, BAND_DIAGS = 64, 64
+# transpose kernel variant: "reg" (register micro-tiles, 64-byte store runs) or
+# "smem" (128-byte runs on both sides through swizzled shared memory)
+TRANSPOSE_VARIANT = os.environ.get("LEGO_TRANSPOSE", "smem")
 
 
 def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
@@ -183,7 +191,7 @@ def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
 
 
 def _remap_program(src_layout, dst_layout, elem_bytes):
-    key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes)
+    key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, TRANSPOSE_VARIANT)
     plan_box = {}
 
     def build():

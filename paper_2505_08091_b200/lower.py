@@ -231,15 +231,17 @@ class TransposePlan:
         self.tx, self.ty = tx, ty
 
 
-def transpose_plan(g: Expr, f: Var, n: int, elem_bytes: int) -> Optional[TransposePlan]:
-    """Register-tiled transpose geometry for a digit-permutation gather."""
+def transpose_plan(g: Expr, f: Var, n: int, elem_bytes: int, x_vectors: int = 4,
+                   y_vectors: int = 8) -> Optional[TransposePlan]:
+    """Warp-tiled transpose geometry for a digit-permutation gather: a warp
+    tile is (x_vectors*V) x (y_vectors*V) elements, V = 16 / elem_bytes."""
     if 16 % elem_bytes:
         return None
     digits = digit_terms(g, f, n)
     if digits is None:
         return None
     v = 16 // elem_bytes
-    tx, ty = 4 * v, 8 * v                 # warp tile: x along dst digit, y along src digit
+    tx, ty = x_vectors * v, y_vectors * v   # x along the dst digit, y along the src digit
     x_lo, x_span, sx = digits[0]
     if sx == 1:
         return None                        # contiguous: the gather path is better

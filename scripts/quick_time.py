@@ -1,40 +1,52 @@
-"""Quick CUDA-event timing of the remap programs (development helper)."""
-import sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch
-import paper_2505_08091_b200 as L
-from paper_2505_08091_b200 import kernels as K
+"""Quick CUDA-event timing of the hot kernels (development helper)."""
+import os
+import sys
 
-def t(fn, iters=20):
-    for _ in range(3): fn()
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2505_08091_b200 as L  # noqa: E402
+from paper_2505_08091_b200 import kernels as K  # noqa: E402
+
+
+def t(fn, iters=30):
+    for _ in range(5):
+        fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    best = 1e9
+    s.record()
     for _ in range(iters):
-        s.record(); fn(); e.record(); e.synchronize()
-        best = min(best, s.elapsed_time(e))
-    return best
+        fn()
+    e.record()
+    e.synchronize()
+    return s.elapsed_time(e) / iters
 
-cases = [
- ("cfg1 tiled fp32", "GroupBy([4096,4096]).OrderBy(RegP([128,32,128,32],[1,3,2,4]))", torch.float32, 8),
- ("cfg2 transpose bf16", "GroupBy([16384,16384]).OrderBy(Col(16384,16384))", torch.bfloat16, 1),
- ("cfg2 transpose fp32", "GroupBy([16384,16384]).OrderBy(Col(16384,16384))", torch.float32, 1),
- ("cfg4 antidiag int32", "GroupBy([16384,16384]).OrderBy(GenP([16384,16384], antidiag))", torch.int32, 1),
-]
-for name, dsl, dt, batch in cases:
-    g = L.parse_layout(dsl)
-    n = g.size
-    src = torch.randn(batch, n, device="cuda").to(dt)
-    out = torch.empty_like(src)
-    for direction in ("scatter", "gather"):
-        a, b = (None, g) if direction == "scatter" else (g, None)
-        ms = t(lambda: K.remap(src, a, b, out=out))
-        gbs = 2 * src.numel() * src.element_size() / ms / 1e6
-        print(f"{name:24s} {direction:8s} {ms*1e3:9.1f} us  {gbs:8.1f} GB/s  plan={K.remap_plan(a, b, src.element_size())}", flush=True)
-    ms = t(lambda: K.apply_map(g, out=torch.empty(n, dtype=torch.int32, device='cuda')))
-    print(f"{name:24s} apply_map {ms*1e3:9.1f} us  {4*n/ms/1e6:8.1f} GB/s (write)", flush=True)
-x = torch.randn(8192, 8192, device="cuda")
-ms = t(lambda: K.softmax(x))
-print(f"softmax 8192^2 {ms*1e3:.1f} us {2*x.numel()*4/ms/1e6:.1f} GB/s")
-ms = t(lambda: src.clone())
-print("copy", ms)
+
+which = sys.argv[1:] or ["transpose", "band", "nw"]
+if "transpose" in which:
+    g = L.parse_layout("GroupBy([16384,16384]).OrderBy(Col(16384,16384))")
+    for dt in (torch.bfloat16, torch.float32, torch.uint8):
+        src = torch.randint(0, 100, (16384 * 16384,), device="cuda").to(dt)
+        out = torch.empty_like(src)
+        for var in ("reg", "smem"):
+            K.TRANSPOSE_VARIANT = var
+            for a, b in ((None, g), (g, None)):
+                ms = t(lambda: K.remap(src, a, b, out=out))
+                print(f"transpose {str(dt):15s} {var:5s} {'scatter' if a is None else 'gather':8s} "
+                      f"{ms*1e3:8.1f} us {2*src.numel()*src.element_size()/ms/1e6:8.1f} GB/s", flush=True)
+    K.TRANSPOSE_VARIANT = "smem"
+if "band" in which:
+    g = L.parse_layout("GroupBy([16384,16384]).OrderBy(GenP([16384,16384], antidiag))")
+    for dt in (torch.int32, torch.bfloat16):
+        src = torch.randint(0, 100, (16384 * 16384,), device="cuda").to(dt)
+        out = torch.empty_like(src)
+        for a, b in ((None, g), (g, None)):
+            ms = t(lambda: K.remap(src, a, b, out=out))
+            print(f"band {str(dt):15s} {'scatter' if a is None else 'gather':8s} {ms*1e3:8.1f} us "
+                  f"{2*src.numel()*src.element_size()/ms/1e6:8.1f} GB/s", flush=True)
+if "nw" in which:
+    for n in (4096, 16384):
+        sim = torch.randint(-10, 11, (n, n), device="cuda", dtype=torch.int32)
+        score = torch.empty(n + 1, n + 1, device="cuda", dtype=torch.int32)
+        ms = t(lambda: K.nw_score(sim, 10, out=score), iters=5)
+        print(f"nw n={n} {ms*1e3:9.1f} us {n*n/ms/1e6:8.1f} GCUPS", flush=True)
