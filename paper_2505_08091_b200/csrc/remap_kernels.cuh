@@ -242,22 +242,37 @@ LEGO_GLOBAL void __launch_bounds__(128) lego_remap(const unsigned char* __restri
 LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
                                                    unsigned char* __restrict__ dst,
                                                    long long src_stride, long long dst_stride) {
+    // LEGO_TPW warp tiles per warp: every tile's loads are issued before the
+    // first transpose, so each lane keeps TPW*V 16-byte loads in flight
+#ifndef LEGO_TPW
+#define LEGO_TPW 1
+#endif
     const int lane = threadIdx.x & 31;
-    const long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (t >= gen::TILES) return;
+    const long long t0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * LEGO_TPW;
+    if (t0 >= gen::TILES) return;
     const unsigned char* s = src + (long long)blockIdx.y * src_stride * LEGO_ELEM;
     unsigned char* d = dst + (long long)blockIdx.y * dst_stride * LEGO_ELEM;
-    long long f0, s0;
-    gen::origin(t, f0, s0);
     const int yg = lane & 7, xg = lane >> 3;
-    const unsigned char* sp = s + (s0 + (long long)(xg * LEGO_V) * gen::SX + yg * LEGO_V) * LEGO_ELEM;
-    lego_v16 rows[LEGO_V], cols[LEGO_V];
+    long long f0[LEGO_TPW];
+    lego_v16 rows[LEGO_TPW][LEGO_V];
 #pragma unroll
-    for (int r = 0; r < LEGO_V; ++r) rows[r] = lego_ld16(sp + (long long)r * gen::SX * LEGO_ELEM);
-    lego_transpose(rows, cols);
-    unsigned char* dp = d + (f0 + (long long)(yg * LEGO_V) * gen::DY + xg * LEGO_V) * LEGO_ELEM;
+    for (int u = 0; u < LEGO_TPW; ++u) {
+        if (t0 + u >= gen::TILES) break;
+        long long s0;
+        gen::origin(t0 + u, f0[u], s0);
+        const unsigned char* sp = s + (s0 + (long long)(xg * LEGO_V) * gen::SX + yg * LEGO_V) * LEGO_ELEM;
 #pragma unroll
-    for (int c = 0; c < LEGO_V; ++c) lego_st16(dp + (long long)c * gen::DY * LEGO_ELEM, cols[c]);
+        for (int r = 0; r < LEGO_V; ++r) rows[u][r] = lego_ld16(sp + (long long)r * gen::SX * LEGO_ELEM);
+    }
+#pragma unroll
+    for (int u = 0; u < LEGO_TPW; ++u) {
+        if (t0 + u >= gen::TILES) break;
+        lego_v16 cols[LEGO_V];
+        lego_transpose(rows[u], cols);
+        unsigned char* dp = d + (f0[u] + (long long)(yg * LEGO_V) * gen::DY + xg * LEGO_V) * LEGO_ELEM;
+#pragma unroll
+        for (int c = 0; c < LEGO_V; ++c) lego_st16(dp + (long long)c * gen::DY * LEGO_ELEM, cols[c]);
+    }
 }
 #endif  // LEGO_SMEM
 #endif
@@ -287,10 +302,20 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
     const int n = gen::NN;
     const lego_e* s = reinterpret_cast<const lego_e*>(src) + (long long)blockIdx.y * src_stride;
     lego_e* d = reinterpret_cast<lego_e*>(dst) + (long long)blockIdx.y * dst_stride;
+#if LEGO_BAND_ORDER == 0
+    // row-block major: consecutive CTAs walk the diagonals of one row block
     const int ri = blockIdx.x / gen::KBLOCKS;
     const int kk = blockIdx.x - ri * gen::KBLOCKS;
     const int i0 = ri * BR;
     const int t0 = (i0 / BK + kk) * BK;
+#else
+    // diagonal-block major: consecutive CTAs walk the row blocks of one band, so
+    // the diagonal runs they write continue each other (L2 merges the seams)
+    const int tb = blockIdx.x / (gen::NN / BR);
+    const int i0 = (blockIdx.x - tb * (gen::NN / BR)) * BR;
+    const int t0 = tb * BK;
+    if (i0 > t0 + BK - 1) return;                      // rows below the band's reach
+#endif
     if (t0 > i0 + BR - 1 + n - 1) return;             // band right of the matrix
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // base position of each diagonal's run: pos(i, t-i) = base_t + i

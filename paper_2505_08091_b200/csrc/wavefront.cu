@@ -134,8 +134,10 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
             if (w > 0) {
                 const int need = min((k + 1) * TILE, n);
                 if (lane == 0) {
-                    while (ld_acquire(left_prog) < need) {
+                    // relaxed polling (no L1 invalidation per probe), one acquire at the end
+                    while (*reinterpret_cast<const volatile int*>(left_prog) < need) {
                     }
+                    (void)ld_acquire(left_prog);
                 }
                 __syncwarp();
                 const int row = k * TILE + lane;
@@ -172,11 +174,17 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                                          CPL * lane) = make_int4(h[0], h[1], h[2], h[3]);
             }
             left_prev = left;
-            // block k completes at step 32k + 62: flush its rows, publish the boundary column
+            // block k completes at step 32k + 62: publish the boundary column first (the
+            // release must not wait behind the row stores), then flush the rows
             if ((s & (TILE - 1)) == TILE - 2 && s >= 2 * TILE - 2) {
                 const int k = (s - (2 * TILE - 2)) / TILE;
                 __syncwarp();
                 const int32_t* src = s_out + (k & 1) * BLOCK_ELEMS;
+                const int brow = k * TILE + lane;
+                if (brow < n) my_bnd[brow] = src[lane * STRIP + STRIP - 1];
+                __threadfence();                     // each lane's boundary value is visible GPU-wide
+                __syncwarp();
+                if (lane == 0) st_release(my_prog, min((k + 1) * TILE, n));
                 for (int r = 0; r < TILE; ++r) {
                     const int row = k * TILE + r;
                     if (row >= n) break;
@@ -187,10 +195,7 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                         if (col0 + c < n) dst[c] = src[r * STRIP + c];
                     }
                 }
-                const int brow = k * TILE + lane;
-                if (brow < n) my_bnd[brow] = src[lane * STRIP + STRIP - 1];
                 __syncwarp();
-                if (lane == 0) st_release(my_prog, min((k + 1) * TILE, n));
             }
             // next step reads row i + 1; a new block enters when lane 0 crosses into it
             if (((s + 1) & (TILE - 1)) == 0 && (s + 1) < n_pad) enter_block((s + 1) / TILE);

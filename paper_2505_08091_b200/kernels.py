@@ -123,7 +123,9 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
         raise UnsupportedNode(f"destination size {n_dst} is not a multiple of {vec} elements "
                               f"({elem_bytes}-byte elements, 16-byte vectors)")
     if not masked:
-        smem_variant = TRANSPOSE_VARIANT == "smem"
+        variant = TRANSPOSE_VARIANT or ("reg" if elem_bytes == 2 else "smem")
+        smem_variant = variant == "smem"
+        tpw = 2 if variant == "reg2" else 1
         tp = lower.transpose_plan(g, f, n_dst, elem_bytes, 8 if smem_variant else 4, 8)
         if tp is not None:
             body = codegen.constant("N", n_dst) + codegen.constant("TILES", tp.tiles)
@@ -133,14 +135,14 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
             warps = 4 if smem_variant else 8
             v = 16 // elem_bytes
             smem = warps * 8 * v * 8 * 16 if smem_variant else 0
+            per_cta = warps * tpw
             info = runtime.ProgramInfo(kind=runtime.KIND_TRANSPOSE, elem_bytes=elem_bytes, n=n_dst,
-                                       units=(tp.tiles + warps - 1) // warps, unit_threads=32,
+                                       units=(tp.tiles + per_cta - 1) // per_cta, unit_threads=32,
                                        block=32 * warps, smem_bytes=smem)
             src = _assemble(body, {"LEGO_KIND": 2, "LEGO_ELEM": elem_bytes,
-                                   "LEGO_SMEM": int(smem_variant)})
+                                   "LEGO_SMEM": int(smem_variant), "LEGO_TPW": tpw})
             return RemapPlan(runtime.KIND_TRANSPOSE, n_dst, n_src, elem_bytes, False, False, src,
-                             info, f"tile {tp.tx}x{tp.ty}{' smem' if smem_variant else ''}, "
-                                   f"SX={tp.sx}, DY={tp.dy}")
+                             info, f"tile {tp.tx}x{tp.ty} {variant}, SX={tp.sx}, DY={tp.dy}")
     width = 1 if masked else lower.contiguous_width(g, f, n_dst, widths=(vec,))
     contig = width >= vec
     body = codegen.constant("N", n_dst)
@@ -158,9 +160,13 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
 
 
 BAND_ROWS, BAND_DIAGS = 64, 64
-# transpose kernel variant: "reg" (register micro-tiles, 64-byte store runs) or
-# "smem" (128-byte runs on both sides through swizzled shared memory)
-TRANSPOSE_VARIANT = os.environ.get("LEGO_TRANSPOSE", "smem")
+# transpose kernel variant: "reg" (register micro-tiles, 64-byte store runs),
+# "reg2" (two tiles per warp in flight) or "smem" (128-byte runs on both sides
+# through swizzled shared memory); empty = per element size, as measured on
+# B200 (scripts/quick_time.py): reg for 2-byte elements, smem otherwise
+TRANSPOSE_VARIANT = os.environ.get("LEGO_TRANSPOSE", "")
+# band tile order: 0 row-block major, 1 diagonal-block major, -1 = per direction
+BAND_ORDER = int(os.environ.get("LEGO_BAND_ORDER", "-1"))
 
 
 def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
@@ -181,17 +187,23 @@ def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
     kblocks = (n + BAND_ROWS + BAND_DIAGS - 2) // BAND_DIAGS + 1
     body = codegen.constant("NN", n) + codegen.constant("KBLOCKS", kblocks)
     body += codegen.generate("pos_of", [x], {"p": pos}).source
-    units = (n // BAND_ROWS) * kblocks
+    order = BAND_ORDER if BAND_ORDER >= 0 else (1 if direction == 0 else 0)
+    if order == 0:
+        units = (n // BAND_ROWS) * kblocks
+    else:
+        units = ((2 * n - 1 + BAND_DIAGS - 1) // BAND_DIAGS) * (n // BAND_ROWS)
     info = runtime.ProgramInfo(kind=runtime.KIND_BAND, elem_bytes=elem_bytes, n=n * n, units=units,
                                unit_threads=256, block=256, smem_bytes=0)
-    src = _assemble(body, {"LEGO_KIND": 3, "LEGO_ELEM": elem_bytes, "LEGO_DIR": direction})
+    src = _assemble(body, {"LEGO_KIND": 3, "LEGO_ELEM": elem_bytes, "LEGO_DIR": direction,
+                           "LEGO_BAND_ORDER": order})
     return RemapPlan(runtime.KIND_BAND, n * n, n * n, elem_bytes, False, False, src, info,
-                     f"band {BAND_ROWS} rows x {BAND_DIAGS} diagonals, "
+                     f"band {BAND_ROWS} rows x {BAND_DIAGS} diagonals, order {order}, "
                      f"{'scatter' if direction == 0 else 'gather'}")
 
 
 def _remap_program(src_layout, dst_layout, elem_bytes):
-    key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, TRANSPOSE_VARIANT)
+    key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, TRANSPOSE_VARIANT,
+           BAND_ORDER)
     plan_box = {}
 
     def build():

@@ -1,4 +1,4 @@
-"""Quick CUDA-event timing of the hot kernels (development helper)."""
+"""Quick CUDA-event timing of the hot kernels and their variants (development helper)."""
 import os
 import sys
 
@@ -28,22 +28,25 @@ if "transpose" in which:
     for dt in (torch.bfloat16, torch.float32, torch.uint8):
         src = torch.randint(0, 100, (16384 * 16384,), device="cuda").to(dt)
         out = torch.empty_like(src)
-        for var in ("reg", "smem"):
+        for var in ("reg", "reg2", "smem"):
             K.TRANSPOSE_VARIANT = var
-            for a, b in ((None, g), (g, None)):
+            for a, b in ((None, g),):
                 ms = t(lambda: K.remap(src, a, b, out=out))
                 print(f"transpose {str(dt):15s} {var:5s} {'scatter' if a is None else 'gather':8s} "
                       f"{ms*1e3:8.1f} us {2*src.numel()*src.element_size()/ms/1e6:8.1f} GB/s", flush=True)
-    K.TRANSPOSE_VARIANT = "smem"
+    K.TRANSPOSE_VARIANT = ""
 if "band" in which:
     g = L.parse_layout("GroupBy([16384,16384]).OrderBy(GenP([16384,16384], antidiag))")
     for dt in (torch.int32, torch.bfloat16):
         src = torch.randint(0, 100, (16384 * 16384,), device="cuda").to(dt)
         out = torch.empty_like(src)
-        for a, b in ((None, g), (g, None)):
-            ms = t(lambda: K.remap(src, a, b, out=out))
-            print(f"band {str(dt):15s} {'scatter' if a is None else 'gather':8s} {ms*1e3:8.1f} us "
-                  f"{2*src.numel()*src.element_size()/ms/1e6:8.1f} GB/s", flush=True)
+        for order in (0, 1):
+            K.BAND_ORDER = order
+            for a, b in ((None, g), (g, None)):
+                ms = t(lambda: K.remap(src, a, b, out=out))
+                print(f"band {str(dt):15s} order {order} {'scatter' if a is None else 'gather':8s} "
+                      f"{ms*1e3:8.1f} us {2*src.numel()*src.element_size()/ms/1e6:8.1f} GB/s", flush=True)
+    K.BAND_ORDER = -1
 if "nw" in which:
     for n in (4096, 16384):
         sim = torch.randint(-10, 11, (n, n), device="cuda", dtype=torch.int32)
