@@ -14,15 +14,14 @@
 //    order of the paper's NW kernel.  The value from the
 //    left arrives by warp shuffle, the up and diagonal values are the lane's
 //    own previous row: the per-step critical path is one shuffle plus a
-//    4-cell max/add chain.  Everything else is off that path:
-//  * sim is staged 32 rows x 128 columns at a time by cp.async two blocks
-//    ahead (4 buffers) and each lane's next 16-byte sim vector is read from
-//    shared memory one step early;
-//  * results go through a 32 x 128 tile and leave as coalesced row segments
-//    once a block of 32 rows is complete; at that point the strip's last
-//    column for those rows is copied to a global boundary array and
-//    published with one st.release, which the right neighbour polls with
-//    ld.acquire once per 32 rows.
+//    4-cell max/add chain, and the step body is branch-free (steps are
+//    grouped 32 at a time so all bookkeeping happens once per block);
+//  * sim is staged 32 rows x 128 columns at a time by cp.async one block
+//    ahead into a 4-block ring, read back one step early along the
+//    anti-diagonal (16-byte, conflict-free); results go to a 2-block ring and
+//    leave as coalesced row segments once a block is complete; the strip's
+//    last column is then published to a global boundary array with one
+//    st.release, which the right neighbour polls once per 32 rows.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -31,14 +30,13 @@
 
 namespace {
 
-constexpr int TILE = 32;                 // rows per staged block
+constexpr int TILE = 32;                 // rows per block
 constexpr int CPL = 4;                   // columns per lane
 constexpr int STRIP = 32 * CPL;          // columns per warp strip
-constexpr int SIM_BUFS = 4;
-constexpr int OUT_BUFS = 2;
-constexpr int BLOCK_ELEMS = TILE * STRIP;
-constexpr int BND_RING = 64;
-constexpr int SMEM_BYTES = (SIM_BUFS + OUT_BUFS) * BLOCK_ELEMS * 4 + BND_RING * 4;
+constexpr int SIM_ROWS = 4 * TILE;       // sim ring: 4 blocks
+constexpr int OUT_ROWS = 2 * TILE;       // out ring: 2 blocks
+constexpr int BND_RING = 2 * TILE;
+constexpr int SMEM_BYTES = (SIM_ROWS + OUT_ROWS) * STRIP * 4 + BND_RING * 4;
 
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
@@ -48,17 +46,28 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
-                 :: "r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;"
-                 :: "r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ int4 lds128(uint32_t a) {
+    int4 v;
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, int x, int y, int z, int w) {
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" :: "r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ int lds32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 
 __global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long long batch) {
     const long long w = n + 1;
@@ -72,39 +81,107 @@ __global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long
     }
 }
 
-// stage sim rows [32k, 32k+32) of the strip into buf (one cp.async group; empty past the end)
-__device__ __forceinline__ void stage_sim(int32_t* buf, const int32_t* simb, int n, int k, int col0, int lane,
-                                          bool vec_ok) {
+struct Strip {
+    const int32_t* simb;
+    int32_t* sc;
+    int32_t* my_bnd;
+    const int32_t* left_bnd;
+    int* my_prog;
+    const int* left_prog;
+    int n, p, w, col0, lane;
+    bool vec_ok;
+    uint32_t sim_base, out_base, bnd_base;   // shared-window addresses
+    int32_t* out_gen;                        // generic pointer of the out ring
+};
+
+// stage sim rows [32k, 32k+32) into ring block k % 4 (one cp.async group)
+__device__ __forceinline__ void stage_sim(const Strip& st, int k) {
+    const int rb = (k & 3) * TILE;
     for (int r = 0; r < TILE; ++r) {
         const int row = k * TILE + r;
-        if (row >= n) break;
-        const int32_t* src = simb + (long long)row * n + col0;
-        int32_t* dst = buf + r * STRIP;
-        if (vec_ok) {
-            if (col0 + CPL * lane < n) cp_async16(dst + CPL * lane, src + CPL * lane);
+        if (row >= st.n) break;
+        const int32_t* src = st.simb + (long long)row * st.n + st.col0;
+        const uint32_t dst = st.sim_base + (uint32_t)((rb + r) * STRIP) * 4u;
+        if (st.vec_ok) {
+            if (st.col0 + CPL * st.lane < st.n) cp_async16(dst + 16u * st.lane, src + CPL * st.lane);
         } else {
 #pragma unroll
             for (int q = 0; q < CPL; ++q) {
-                const int c = q * 32 + lane;
-                if (col0 + c < n) cp_async4(dst + c, src + c);
+                const int c = q * 32 + st.lane;
+                if (st.col0 + c < st.n) cp_async4(dst + 4u * c, src + c);
             }
         }
     }
     cp_async_commit();
 }
 
+// block k enters: sim block k landed (block k+1 in flight), boundary rows of
+// block k in the ring (analytic column 0 for the first strip)
+__device__ __forceinline__ void enter_block(const Strip& st, int k, int nblocks) {
+    if (k + 1 < nblocks) {
+        stage_sim(st, k + 1);
+        cp_async_wait_1();
+    } else {
+        cp_async_wait_all();
+    }
+    const int row = k * TILE + st.lane;
+    int32_t v;
+    if (st.w > 0) {
+        const int need = min((k + 1) * TILE, st.n);
+        if (st.lane == 0) {
+            while (*reinterpret_cast<const volatile int*>(st.left_prog) < need) {
+            }
+            (void)ld_acquire(st.left_prog);
+        }
+        __syncwarp();
+        v = row < st.n ? __ldcg(st.left_bnd + row) : 0;
+    } else {
+        v = -(row + 1) * st.p;               // S[row+1][0]
+    }
+    asm volatile("st.shared.b32 [%0], %1;" :: "r"(st.bnd_base + 4u * (row & (BND_RING - 1))), "r"(v)
+                 : "memory");
+    __syncwarp();
+}
+
+// block k is complete: publish its boundary column, then write its rows out
+__device__ __forceinline__ void flush_block(const Strip& st, int k) {
+    __syncwarp();
+    const int32_t* src = st.out_gen + (k & 1) * TILE * STRIP;
+    const int brow = k * TILE + st.lane;
+    if (brow < st.n) st.my_bnd[brow] = src[st.lane * STRIP + STRIP - 1];
+    __threadfence();
+    __syncwarp();
+    if (st.lane == 0) st_release(st.my_prog, min((k + 1) * TILE, st.n));
+    const long long ld = (long long)st.n + 1;
+    for (int r = 0; r < TILE; ++r) {
+        const int row = k * TILE + r;
+        if (row >= st.n) break;
+        int32_t* dst = st.sc + (long long)(row + 1) * ld + st.col0 + 1;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+            const int c = q * 32 + st.lane;
+            if (st.col0 + c < st.n) dst[c] = src[r * STRIP + c];
+        }
+    }
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(32)
 nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, int p, int strips_per_matrix,
           int total_strips, int* __restrict__ ticket, int* __restrict__ progress, int32_t* __restrict__ bnd) {
     extern __shared__ __align__(16) int32_t smem[];
-    int32_t* s_sim = smem;                                   // [4][32][128]
-    int32_t* s_out = s_sim + SIM_BUFS * BLOCK_ELEMS;         // [2][32][128]
-    int32_t* s_bnd = s_out + OUT_BUFS * BLOCK_ELEMS;         // ring of 64 rows
     const int lane = threadIdx.x;
-    const long long ld = (long long)n + 1;
     const int n_pad = (n + TILE - 1) / TILE * TILE;
     const int nblocks = n_pad / TILE;
-    const bool vec_ok = (n % 4) == 0;
+    Strip st;
+    st.n = n;
+    st.p = p;
+    st.lane = lane;
+    st.vec_ok = (n % 4) == 0;
+    st.sim_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    st.out_base = st.sim_base + SIM_ROWS * STRIP * 4;
+    st.bnd_base = st.out_base + OUT_ROWS * STRIP * 4;
+    st.out_gen = smem + SIM_ROWS * STRIP;
 
     for (;;) {
         int strip = 0;
@@ -112,97 +189,49 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
         strip = __shfl_sync(0xffffffffu, strip, 0);
         if (strip >= total_strips) return;
         const int b = strip / strips_per_matrix;
-        const int w = strip - b * strips_per_matrix;
-        const int32_t* simb = sim + (long long)b * n * n;
-        int32_t* sc = score + (long long)b * ld * ld;
-        int32_t* my_bnd = bnd + (long long)strip * n_pad;
-        const int32_t* left_bnd = my_bnd - n_pad;
-        int* my_prog = progress + strip;
-        const int* left_prog = progress + strip - 1;
-        const int col0 = w * STRIP;
-        const int c_lane = col0 + CPL * lane;                 // first 0-based sim column of this lane
+        st.w = strip - b * strips_per_matrix;
+        st.simb = sim + (long long)b * n * n;
+        st.sc = score + (long long)b * ((long long)n + 1) * ((long long)n + 1);
+        st.my_bnd = bnd + (long long)strip * n_pad;
+        st.left_bnd = st.my_bnd - n_pad;
+        st.my_prog = progress + strip;
+        st.left_prog = progress + strip - 1;
+        st.col0 = st.w * STRIP;
+        const int c_lane = st.col0 + CPL * lane;
 
-        // block boundary event for block k: its sim landed, block k+1 in flight,
-        // left boundary rows of block k in the ring
-        auto enter_block = [&](int k) {
-            if (k + 1 < nblocks) {
-                stage_sim(s_sim + ((k + 1) & (SIM_BUFS - 1)) * BLOCK_ELEMS, simb, n, k + 1, col0, lane, vec_ok);
-                cp_async_wait_1();
-            } else {
-                cp_async_wait_all();
-            }
-            if (w > 0) {
-                const int need = min((k + 1) * TILE, n);
-                if (lane == 0) {
-                    // relaxed polling (no L1 invalidation per probe), one acquire at the end
-                    while (*reinterpret_cast<const volatile int*>(left_prog) < need) {
-                    }
-                    (void)ld_acquire(left_prog);
-                }
-                __syncwarp();
-                const int row = k * TILE + lane;
-                if (row < n) s_bnd[row & (BND_RING - 1)] = __ldcg(left_bnd + row);
-            }
-            __syncwarp();
-        };
-
-        stage_sim(s_sim, simb, n, 0, col0, lane, vec_ok);
-        enter_block(0);
-
-        int32_t h[CPL];
-#pragma unroll
-        for (int k = 0; k < CPL; ++k) h[k] = -(c_lane + k + 1) * p;   // S[0][c+1]
-        int32_t left_prev = -c_lane * p;                               // S[0][c_lane]
+        stage_sim(st, 0);
+        int32_t h0 = -(c_lane + 1) * p, h1 = -(c_lane + 2) * p, h2 = -(c_lane + 3) * p,
+                h3 = -(c_lane + 4) * p;                    // S[0][c+1..c+4]
+        int32_t left_prev = -c_lane * p;                    // S[0][c_lane]
         int4 sv = make_int4(0, 0, 0, 0);
-        if (lane == 0) sv = *reinterpret_cast<const int4*>(s_sim);    // row 0 for lane 0
 
-        for (int s = 0; s < n_pad + TILE - 1; ++s) {
-            const int i = s - lane;
-            int32_t left = __shfl_up_sync(0xffffffffu, h[CPL - 1], 1);   // S[i+1][c_lane] from lane-1
-            if (lane == 0) left = w == 0 ? -(i + 1) * p : s_bnd[i & (BND_RING - 1)];
-            if (i >= 0 && i < n) {
-                const int32_t svals[CPL] = {sv.x, sv.y, sv.z, sv.w};
-                int32_t diag = left_prev, lf = left;
-#pragma unroll
-                for (int k = 0; k < CPL; ++k) {
-                    const int32_t v = max(diag + svals[k], max(h[k], lf) - p);
-                    diag = h[k];
-                    h[k] = v;
-                    lf = v;
+        for (int k = 0; k <= nblocks + 1; ++k) {
+            if (k >= 2) flush_block(st, k - 2);
+            if (k > nblocks) break;
+            if (k < nblocks) enter_block(st, k, nblocks);
+            // this step's sim vector (lane 0's row just entered; others re-read resident rows)
+            sv = lds128(st.sim_base + (uint32_t)((((k * TILE - lane) & (SIM_ROWS - 1)) * STRIP) * 4) + 16u * lane);
+#pragma unroll 4
+            for (int u = 0; u < TILE; ++u) {
+                const int s = k * TILE + u;
+                const int i = s - lane;                  // row of this lane (may be < 0 or >= n)
+                const int shl = __shfl_up_sync(0xffffffffu, h3, 1);
+                const int bv = lds32(st.bnd_base + 4u * (s & (BND_RING - 1)));
+                const int left = lane == 0 ? bv : shl;
+                int v0 = max(left_prev + sv.x, max(h0, left) - p);
+                int v1 = max(h0 + sv.y, max(h1, v0) - p);
+                int v2 = max(h1 + sv.z, max(h2, v1) - p);
+                int v3 = max(h2 + sv.w, max(h3, v2) - p);
+                const bool started = k > 0 || i >= 0;   // lanes start one step apart
+                if (started) {
+                    h0 = v0; h1 = v1; h2 = v2; h3 = v3;
+                    left_prev = left;
                 }
-                *reinterpret_cast<int4*>(s_out + ((i >> 5) & 1) * BLOCK_ELEMS + (i & (TILE - 1)) * STRIP +
-                                         CPL * lane) = make_int4(h[0], h[1], h[2], h[3]);
+                sts128(st.out_base + (uint32_t)(((i & (OUT_ROWS - 1)) * STRIP) * 4) + 16u * lane, h0, h1, h2, h3);
+                // next row's sim vector (its block is resident: entered at the block start)
+                const int ni = i + 1;
+                sv = lds128(st.sim_base + (uint32_t)(((ni & (SIM_ROWS - 1)) * STRIP) * 4) + 16u * lane);
             }
-            left_prev = left;
-            // block k completes at step 32k + 62: publish the boundary column first (the
-            // release must not wait behind the row stores), then flush the rows
-            if ((s & (TILE - 1)) == TILE - 2 && s >= 2 * TILE - 2) {
-                const int k = (s - (2 * TILE - 2)) / TILE;
-                __syncwarp();
-                const int32_t* src = s_out + (k & 1) * BLOCK_ELEMS;
-                const int brow = k * TILE + lane;
-                if (brow < n) my_bnd[brow] = src[lane * STRIP + STRIP - 1];
-                __threadfence();                     // each lane's boundary value is visible GPU-wide
-                __syncwarp();
-                if (lane == 0) st_release(my_prog, min((k + 1) * TILE, n));
-                for (int r = 0; r < TILE; ++r) {
-                    const int row = k * TILE + r;
-                    if (row >= n) break;
-                    int32_t* dst = sc + (long long)(row + 1) * ld + col0 + 1;
-#pragma unroll
-                    for (int q = 0; q < CPL; ++q) {
-                        const int c = q * 32 + lane;
-                        if (col0 + c < n) dst[c] = src[r * STRIP + c];
-                    }
-                }
-                __syncwarp();
-            }
-            // next step reads row i + 1; a new block enters when lane 0 crosses into it
-            if (((s + 1) & (TILE - 1)) == 0 && (s + 1) < n_pad) enter_block((s + 1) / TILE);
-            const int ni = i + 1;
-            if (ni >= 0 && ni < n)
-                sv = *reinterpret_cast<const int4*>(s_sim + ((ni >> 5) & (SIM_BUFS - 1)) * BLOCK_ELEMS +
-                                                    (ni & (TILE - 1)) * STRIP + CPL * lane);
         }
         cp_async_wait_all();
         __syncwarp();
@@ -242,7 +271,7 @@ extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long cap = 2LL * sms;       // two strips per SM fit the staging buffers
+    const long long cap = 2LL * sms;       // two strips per SM fit the staging rings
     const long long ctas = total < cap ? total : cap;
     nw_strips<<<(unsigned)ctas, 32, SMEM_BYTES, st>>>(sim, score, (int)n, penalty, strips, (int)total, ticket,
                                                       progress, bnd);
