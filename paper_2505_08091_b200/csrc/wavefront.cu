@@ -210,27 +210,34 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
             if (k > nblocks) break;
             if (k < nblocks) enter_block(st, k, nblocks);
             // this step's sim vector (lane 0's row just entered; others re-read resident rows)
-            sv = lds128(st.sim_base + (uint32_t)((((k * TILE - lane) & (SIM_ROWS - 1)) * STRIP) * 4) + 16u * lane);
-#pragma unroll 4
+            const int4* sim_ring = reinterpret_cast<const int4*>(smem) + lane;          // row stride STRIP/4
+            int4* out_ring = reinterpret_cast<int4*>(st.out_gen) + lane;
+            const int* bnd_ring = st.out_gen + OUT_ROWS * STRIP;
+            sv = sim_ring[((k * TILE - lane) & (SIM_ROWS - 1)) * (STRIP / 4)];
+#pragma unroll
             for (int u = 0; u < TILE; ++u) {
                 const int s = k * TILE + u;
                 const int i = s - lane;                  // row of this lane (may be < 0 or >= n)
+                // everything not fed by the left neighbour first (overlaps the shuffle):
+                // x_c = max(diag_c + sim_c, up_c - p); the chain is then v_c = max(v_{c-1} - p, x_c)
+                const int x0 = max(left_prev + sv.x, h0 - p);
+                const int x1 = max(h0 + sv.y, h1 - p);
+                const int x2 = max(h1 + sv.z, h2 - p);
+                const int x3 = max(h2 + sv.w, h3 - p);
+                const int bv = bnd_ring[s & (BND_RING - 1)];
                 const int shl = __shfl_up_sync(0xffffffffu, h3, 1);
-                const int bv = lds32(st.bnd_base + 4u * (s & (BND_RING - 1)));
                 const int left = lane == 0 ? bv : shl;
-                int v0 = max(left_prev + sv.x, max(h0, left) - p);
-                int v1 = max(h0 + sv.y, max(h1, v0) - p);
-                int v2 = max(h1 + sv.z, max(h2, v1) - p);
-                int v3 = max(h2 + sv.w, max(h3, v2) - p);
-                const bool started = k > 0 || i >= 0;   // lanes start one step apart
-                if (started) {
+                const int v0 = max(left - p, x0);
+                const int v1 = max(v0 - p, x1);
+                const int v2 = max(v1 - p, x2);
+                const int v3 = max(v2 - p, x3);
+                if (k > 0 || i >= 0) {                   // lanes start one step apart
                     h0 = v0; h1 = v1; h2 = v2; h3 = v3;
                     left_prev = left;
                 }
-                sts128(st.out_base + (uint32_t)(((i & (OUT_ROWS - 1)) * STRIP) * 4) + 16u * lane, h0, h1, h2, h3);
+                out_ring[(i & (OUT_ROWS - 1)) * (STRIP / 4)] = make_int4(h0, h1, h2, h3);
                 // next row's sim vector (its block is resident: entered at the block start)
-                const int ni = i + 1;
-                sv = lds128(st.sim_base + (uint32_t)(((ni & (SIM_ROWS - 1)) * STRIP) * 4) + 16u * lane);
+                sv = sim_ring[((i + 1) & (SIM_ROWS - 1)) * (STRIP / 4)];
             }
         }
         cp_async_wait_all();

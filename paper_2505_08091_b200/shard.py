@@ -1,0 +1,163 @@
+"""Multi-GPU sharding of independent layout work (one process per GPU).
+
+The LEGO hot path is embarrassingly parallel over independent matrices (a
+batch) and, for row-local kernels, over rows: every shard is processed by
+its own GPU with no data-path collective.  NCCL appears only where a result
+has to cross shards:
+
+* :func:`gather_shards` -- reassemble a batch-sharded result on every rank
+  (``all_gather_into_tensor``; ragged shards are padded and trimmed);
+* :func:`transpose_rows` -- a *single* matrix whose rows are split across
+  ranks, remapped into a layout that needs other ranks' rows (the
+  column-major ``Col`` layout): one ``all_to_all_single`` of row-block x
+  column-block tiles, then each rank finishes with local LEGO remaps.
+
+All functions take ``compute=`` so the host logic is testable on CPU with
+the ``gloo`` backend (tests/test_shard.py injects the oracle); the default
+compute is the GPU kernel of :mod:`.kernels`.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+from .errors import ShapeMismatch
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    """Contiguous split of ``total`` independent items over ``world`` ranks."""
+
+    total: int
+    world: int
+    rank: int
+
+    @property
+    def per_rank(self) -> int:
+        return math.ceil(self.total / self.world) if self.world else 0
+
+    @property
+    def start(self) -> int:
+        return min(self.total, self.rank * self.per_rank)
+
+    @property
+    def stop(self) -> int:
+        return min(self.total, self.start + self.per_rank)
+
+    @property
+    def count(self) -> int:
+        return self.stop - self.start
+
+    def bounds(self, rank: int):
+        return ShardPlan(self.total, self.world, rank).start, ShardPlan(self.total, self.world, rank).stop
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+def world_and_rank(group=None):
+    dist = _dist()
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def plan(total: int, group=None) -> ShardPlan:
+    world, rank = world_and_rank(group)
+    return ShardPlan(total, world, rank)
+
+
+def local_slice(x, group=None):
+    """This rank's contiguous share of the leading (batch) dimension of x."""
+    p = plan(x.shape[0], group)
+    return x[p.start:p.stop]
+
+
+def sharded(fn: Callable, x, *args, group=None, gather: bool = False, **kw):
+    """Apply ``fn`` (e.g. ``kernels.remap``) to this rank's batch shard; with
+    ``gather=True`` return the full result on every rank."""
+    p = plan(x.shape[0], group)
+    out = fn(x[p.start:p.stop], *args, **kw)
+    return gather_shards(out, p, group) if gather else out
+
+
+def gather_shards(local, p: ShardPlan, group=None):
+    """All-gather equally-padded batch shards and trim to ``p.total``."""
+    import torch
+    dist = _dist()
+    if p.world == 1:
+        return local
+    pad = p.per_rank - local.shape[0]
+    if pad:
+        local = torch.cat([local, local.new_zeros((pad,) + tuple(local.shape[1:]))])
+    full = local.new_empty((p.per_rank * p.world,) + tuple(local.shape[1:]))
+    if hasattr(dist, "all_gather_into_tensor") and local.is_cuda:
+        dist.all_gather_into_tensor(full, local.contiguous(), group=group)
+    else:
+        parts = list(full.chunk(p.world))
+        dist.all_gather(parts, local.contiguous(), group=group)
+        full = torch.cat(parts)
+    return full[:p.total]
+
+
+def transpose_rows(local_rows, n_rows: int, n_cols: int, *, group=None,
+                   compute: Optional[Callable] = None):
+    """Distributed ``Col`` layout of one row-sharded matrix.
+
+    Rank r holds rows [r*R, (r+1)*R) of an (n_rows x n_cols) row-major
+    matrix (R = n_rows / world).  The result in the layout
+    ``GroupBy([n_rows, n_cols]).OrderBy(Col(n_cols, n_rows))`` is the
+    transposed matrix; rank r returns its rows [r*C, (r+1)*C) of that
+    (n_cols x n_rows) array (C = n_cols / world).
+
+    Step 1 (local, LEGO): cut the local rows into ``world`` column blocks,
+    each a contiguous (R x C) tile -- a batched tile_by remap.
+    Step 2 (NCCL): one ``all_to_all_single`` so rank r receives tile r of
+    every rank.  Step 3 (local, LEGO): transpose each received (R x C) tile
+    to (C x R) and lay the tiles side by side.
+    """
+    import torch
+    dist = _dist()
+    world, rank = world_and_rank(group)
+    if n_rows % world or n_cols % world:
+        raise ShapeMismatch(f"{n_rows}x{n_cols} does not split over {world} ranks")
+    R, C = n_rows // world, n_cols // world
+    if local_rows.shape != (R, n_cols):
+        raise ShapeMismatch(f"local rows {tuple(local_rows.shape)} != {(R, n_cols)}")
+    tile_layout, t_layout = _transpose_layouts(R, C, world)
+    run = compute or _gpu_remap
+    # (R, world*C) row-major -> world tiles of (R, C), contiguous per tile
+    tiles = run(local_rows.reshape(-1), None, tile_layout).reshape(world, R * C)
+    recv = torch.empty_like(tiles)
+    if world > 1:
+        dist.all_to_all_single(recv, tiles, group=group)
+    else:
+        recv.copy_(tiles)
+    # recv[q] is tile (rows of rank q) x (my column block): transpose each to (C, R)
+    tt = run(recv, None, t_layout)                          # (world, C*R), each C x R
+    # place tiles side by side: out[c, q*R + r] = tt[q, c*R + r]
+    return run(tt.reshape(-1), None, _sidebyside_layout(R, C, world)).reshape(C, world * R)
+
+
+def _transpose_layouts(R, C, world):
+    from .layout import GroupBy, RegP
+    # logical (r, q, c) of the local (R, world*C) rows -> position q*R*C + r*C + c
+    tile = GroupBy([R, world, C]).order_by(RegP((R, world, C), (2, 1, 3)))
+    # logical (r, c) of an R x C tile -> position c*R + r (column-major)
+    trans = GroupBy([R, C]).order_by(RegP((R, C), (2, 1)))
+    return tile, trans
+
+
+def _sidebyside_layout(R, C, world):
+    from .layout import GroupBy, RegP
+    # logical (q, c, r) of `world` stacked C x R tiles -> position c*world*R + q*R + r
+    return GroupBy([world, C, R]).order_by(RegP((world, C, R), (2, 1, 3)))
+
+
+def _gpu_remap(x, src_layout, dst_layout):
+    from . import kernels
+    return kernels.remap(x, src_layout, dst_layout)

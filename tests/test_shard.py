@@ -1,0 +1,118 @@
+"""Multi-process host logic of the sharding layer: world_size 2 over gloo on
+CPU, with the per-shard compute injected (the GPU kernel is replaced by the
+scalar layout API, itself pinned to the reference by test_frontend.py)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2505_08091_b200 as L
+from paper_2505_08091_b200 import shard
+
+
+def cpu_remap(x, src_layout, dst_layout):
+    """dst[dst.apply(v)] = src[src.apply(v)] with the scalar API (tiny sizes)."""
+    some = src_layout or dst_layout
+    dims = some.dims
+    n = int(np.prod(dims))
+    flat = x.reshape(-1, n)
+    out = torch.empty_like(flat)
+    for v in range(n):
+        idx = []
+        rem = v
+        for d in reversed(dims):
+            idx.append(rem % d)
+            rem //= d
+        idx = tuple(reversed(idx))
+        s = src_layout.apply(idx) if src_layout is not None else v
+        t = dst_layout.apply(idx) if dst_layout is not None else v
+        out[:, t] = flat[:, s]
+    return out.reshape(x.shape[:-1] + (n,)) if x.dim() > 1 else out.reshape(n)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, fn, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fn(rank, world)
+        q.put((rank, None))
+    except Exception as exc:  # noqa: BLE001
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_world(fn, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fn, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    errs = [e for _, e in results if e]
+    assert not errs, errs[0]
+
+
+def _batch_case(rank, world):
+    g = L.parse_layout("GroupBy([8,8]).OrderBy(Col(8,8))")
+    x = torch.arange(5 * 64, dtype=torch.int32).reshape(5, 64)        # 5 items: ragged over 2
+    out = shard.sharded(cpu_remap, x, None, g, gather=True)
+    want = cpu_remap(x, None, g)
+    assert torch.equal(out, want)
+    p = shard.plan(5)
+    assert (p.start, p.stop) == ((0, 3) if rank == 0 else (3, 5))
+
+
+def _transpose_case(rank, world):
+    n_rows, n_cols = 8, 12
+    full = torch.arange(n_rows * n_cols, dtype=torch.int32).reshape(n_rows, n_cols)
+    R = n_rows // world
+    local = full[rank * R:(rank + 1) * R].contiguous()
+    got = shard.transpose_rows(local, n_rows, n_cols, compute=cpu_remap)
+    C = n_cols // world
+    assert torch.equal(got, full.t()[rank * C:(rank + 1) * C])
+    # and it is exactly the LEGO Col layout of the whole matrix
+    g = L.parse_layout(f"GroupBy([{n_rows},{n_cols}]).OrderBy(Col({n_cols},{n_rows}))")
+    whole = cpu_remap(full.reshape(-1), None, g).reshape(n_cols, n_rows)
+    assert torch.equal(got, whole[rank * C:(rank + 1) * C])
+
+
+def test_batch_sharding_with_ragged_gather():
+    run_world(_batch_case)
+
+
+def test_row_sharded_transpose_all_to_all():
+    run_world(_transpose_case)
+
+
+def test_plan_covers_everything():
+    for total in (0, 1, 7, 8, 65537):
+        for world in (1, 2, 4, 8):
+            spans = [shard.ShardPlan(total, world, r) for r in range(world)]
+            covered = sum(p.count for p in spans)
+            assert covered == total
+            assert all(a.stop == b.start for a, b in zip(spans, spans[1:]))
+
+
+def test_single_process_defaults():
+    x = torch.arange(16).reshape(4, 4)
+    assert shard.plan(4).count == 4
+    assert torch.equal(shard.local_slice(x), x)
