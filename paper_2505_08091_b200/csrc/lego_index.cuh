@@ -3,31 +3,29 @@
 // Semantics follow the reference Expr evaluator (pkg/src/lego/expr.py:261-298):
 // floor division, Python-sign modulo (result has the divisor's sign), exact
 // integer square root.  Self-contained (no std headers) so NVRTC can compile
-// it without a CUDA include path.
+// it without a CUDA include path.  The division helpers are templates so a
+// 64-bit numerator with a 32-bit literal divisor (what emit.CUDA_PROFILE
+// prints) computes in the wider type.
 #pragma once
 
 typedef unsigned long long lego_u64;
 typedef long long lego_i64;
 
-static __device__ __forceinline__ long long lego_fdiv(long long a, long long b) {
-    if (b == 0) return 0;                       // unreachable for valid layouts
-    long long q = a / b;
-    return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+template <typename A, typename B>
+static __device__ __forceinline__ auto lego_fdiv(A a, B b) -> decltype(a + b) {
+    typedef decltype(a + b) T;
+    const T x = (T)a, y = (T)b;
+    if (y == 0) return 0;                       // unreachable for valid layouts
+    const T q = x / y;
+    return (x % y != 0 && ((x < 0) != (y < 0))) ? q - 1 : q;
 }
-static __device__ __forceinline__ int lego_fdiv(int a, int b) {
-    if (b == 0) return 0;
-    int q = a / b;
-    return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
-}
-static __device__ __forceinline__ long long lego_fmod(long long a, long long b) {
-    if (b == 0) return 0;
-    long long r = a % b;
-    return (r != 0 && ((r < 0) != (b < 0))) ? r + b : r;
-}
-static __device__ __forceinline__ int lego_fmod(int a, int b) {
-    if (b == 0) return 0;
-    int r = a % b;
-    return (r != 0 && ((r < 0) != (b < 0))) ? r + b : r;
+template <typename A, typename B>
+static __device__ __forceinline__ auto lego_fmod(A a, B b) -> decltype(a + b) {
+    typedef decltype(a + b) T;
+    const T x = (T)a, y = (T)b;
+    if (y == 0) return 0;
+    const T r = x % y;
+    return (r != 0 && ((r < 0) != (y < 0))) ? r + y : r;
 }
 
 // exact floor(sqrt(x)); negative arguments clamp to 0 (only reachable in the
@@ -46,3 +44,6 @@ static __device__ __forceinline__ long long lego_isqrt64(long long x) {
     while ((r + 1) * (r + 1) <= x) ++r;
     return r;
 }
+// overloads used by the `cuda` emit profile (emit.CUDA_PROFILE, template splices)
+static __device__ __forceinline__ int lego_isqrt(int x) { return lego_isqrt32(x); }
+static __device__ __forceinline__ long long lego_isqrt(long long x) { return lego_isqrt64(x); }

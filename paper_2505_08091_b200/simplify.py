@@ -25,6 +25,7 @@ rewrite is sound without sign proofs except where a range test is stated.
 from __future__ import annotations
 
 import math
+import threading
 from typing import Dict, Iterable, Mapping, Optional, Tuple
 
 from .errors import DivisionByZero, UnboundVariable
@@ -267,11 +268,18 @@ def _lin_of(e: Expr) -> Lin:
 
 
 def _term(atom: Expr, mag: int) -> Expr:
-    return atom if mag == 1 else Mul(atom, IntConst(mag))
+    if mag == 1:
+        return atom
+    # expanded variants print coefficient-first (2*i, like expand()); plain
+    # ones keep the stride form that canonical flattening produces (i*8)
+    return Mul(atom, IntConst(mag)) if getattr(_MODE, "factor", True) else Mul(IntConst(mag), atom)
+
+
+_MODE = threading.local()     # factor_gcd switch of the running simplify() call
 
 
 def _build(lin: Lin) -> Expr:
-    if len(lin.terms) > 1:
+    if len(lin.terms) > 1 and getattr(_MODE, "factor", True):
         g = math.gcd(lin.const, *lin.terms.values())
         if g > 1:
             # keep a common factor factored out: 2*(i + j), not i*2 + j*2
@@ -588,31 +596,39 @@ def _digit_atom(base: Expr, lo: int, span: Optional[int]) -> Expr:
 # Public entry points.
 # ---------------------------------------------------------------------------
 
-def simplify(e: Expr, facts: FactSet = EMPTY_FACTS, *, budget: int = DEFAULT_BUDGET) -> Expr:
+def simplify(e: Expr, facts: FactSet = EMPTY_FACTS, *, budget: int = DEFAULT_BUDGET,
+             factor_gcd: bool = True) -> Expr:
     """Semantically equal, usually smaller expression; never raises.
 
     ``budget`` bounds the number of whole-expression normalisation passes
     (each pass is linear in the DAG size); it exists for API parity with the
-    reference, whose budget counts individual rule firings.
+    reference, whose budget counts individual rule firings.  ``factor_gcd``
+    keeps a common constant factor of a sum factored out (``2*(i + j)``);
+    the expanded variants switch it off so they stay fully distributed.
     """
     if budget <= 0:
         return e
     passes = min(budget, 8)
     cur = e
-    for _ in range(passes):
-        try:
-            nxt = _Normaliser(facts).run(cur)
-        except (UnboundVariable, DivisionByZero, ValueError):
-            return cur
-        if nxt == cur:
-            return nxt
-        cur = nxt
-    return cur
+    prev = getattr(_MODE, "factor", True)
+    _MODE.factor = factor_gcd
+    try:
+        for _ in range(passes):
+            try:
+                nxt = _Normaliser(facts).run(cur)
+            except (UnboundVariable, DivisionByZero, ValueError):
+                return cur
+            if nxt == cur:
+                return nxt
+            cur = nxt
+        return cur
+    finally:
+        _MODE.factor = prev
 
 
 def best_variant(e: Expr, facts: FactSet = EMPTY_FACTS, *, budget: int = DEFAULT_BUDGET) -> Expr:
     """Cheaper (by ``op_count``) of ``simplify(e)`` and ``simplify(expand(e))``;
     ties keep the unexpanded form (reference ``simplify.py:635-644``)."""
     plain = simplify(e, facts, budget=budget)
-    alt = simplify(expand(e), facts, budget=budget)
+    alt = simplify(expand(e), facts, budget=budget, factor_gcd=False)
     return alt if op_count(alt) < op_count(plain) else plain
