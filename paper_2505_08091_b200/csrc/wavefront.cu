@@ -55,19 +55,6 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ int4 lds128(uint32_t a) {
-    int4 v;
-    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sts128(uint32_t a, int x, int y, int z, int w) {
-    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" :: "r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
-}
-__device__ __forceinline__ int lds32(uint32_t a) {
-    int v;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
 
 __global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long long batch) {
     const long long w = n + 1;
@@ -96,20 +83,29 @@ struct Strip {
 
 // stage sim rows [32k, 32k+32) into ring block k % 4 (one cp.async group)
 __device__ __forceinline__ void stage_sim(const Strip& st, int k) {
-    const int rb = (k & 3) * TILE;
-    for (int r = 0; r < TILE; ++r) {
-        const int row = k * TILE + r;
-        if (row >= st.n) break;
-        const int32_t* src = st.simb + (long long)row * st.n + st.col0;
-        const uint32_t dst = st.sim_base + (uint32_t)((rb + r) * STRIP) * 4u;
-        if (st.vec_ok) {
-            if (st.col0 + CPL * st.lane < st.n) cp_async16(dst + 16u * st.lane, src + CPL * st.lane);
-        } else {
+    // pointer-walking, fully unrolled: ~3 instructions per row (the issue cost
+    // of this loop competes with the wavefront steps of the same warp)
+    const int rows = min(TILE, st.n - k * TILE);
+    uint32_t dst = st.sim_base + (uint32_t)((k & 3) * TILE * STRIP) * 4u;
+    if (st.vec_ok) {
+        const int32_t* src = st.simb + (long long)k * TILE * st.n + st.col0 + CPL * st.lane;
+        const bool ok = st.col0 + CPL * st.lane < st.n;
+        dst += 16u * st.lane;
 #pragma unroll
-            for (int q = 0; q < CPL; ++q) {
-                const int c = q * 32 + st.lane;
-                if (st.col0 + c < st.n) cp_async4(dst + 4u * c, src + c);
-            }
+        for (int r = 0; r < TILE; ++r) {
+            if (ok && r < rows) cp_async16(dst, src);
+            dst += STRIP * 4u;
+            src += st.n;
+        }
+    } else {
+        const int32_t* src = st.simb + (long long)k * TILE * st.n + st.col0 + st.lane;
+        dst += 4u * st.lane;
+        for (int r = 0; r < rows; ++r) {
+#pragma unroll
+            for (int q = 0; q < CPL; ++q)
+                if (st.col0 + q * 32 + st.lane < st.n) cp_async4(dst + 128u * q, src + 32 * q);
+            dst += STRIP * 4u;
+            src += st.n;
         }
     }
     cp_async_commit();
@@ -153,15 +149,19 @@ __device__ __forceinline__ void flush_block(const Strip& st, int k) {
     __syncwarp();
     if (st.lane == 0) st_release(st.my_prog, min((k + 1) * TILE, st.n));
     const long long ld = (long long)st.n + 1;
-    for (int r = 0; r < TILE; ++r) {
-        const int row = k * TILE + r;
-        if (row >= st.n) break;
-        int32_t* dst = st.sc + (long long)(row + 1) * ld + st.col0 + 1;
+    const int rows = min(TILE, st.n - k * TILE);
+    int32_t* dst = st.sc + (long long)(k * TILE + 1) * ld + st.col0 + 1 + st.lane;
+    const int32_t* s = src + st.lane;
+    bool ok[CPL];
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-            const int c = q * 32 + st.lane;
-            if (st.col0 + c < st.n) dst[c] = src[r * STRIP + c];
-        }
+    for (int q = 0; q < CPL; ++q) ok[q] = st.col0 + q * 32 + st.lane < st.n;
+#pragma unroll 8
+    for (int r = 0; r < rows; ++r) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+            if (ok[q]) dst[32 * q] = s[32 * q];
+        dst += ld;
+        s += STRIP;
     }
     __syncwarp();
 }
