@@ -56,6 +56,17 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
+__device__ __forceinline__ int4 lds128v(uint32_t a) {
+    int4 v;
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds32v(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
 __global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long long batch) {
     const long long w = n + 1;
     const long long total = batch * w;
@@ -203,28 +214,39 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
         int32_t h0 = -(c_lane + 1) * p, h1 = -(c_lane + 2) * p, h2 = -(c_lane + 3) * p,
                 h3 = -(c_lane + 4) * p;                    // S[0][c+1..c+4]
         int32_t left_prev = -c_lane * p;                    // S[0][c_lane]
-        int4 sv = make_int4(0, 0, 0, 0);
 
         for (int k = 0; k <= nblocks + 1; ++k) {
             if (k >= 2) flush_block(st, k - 2);
             if (k > nblocks) break;
             if (k < nblocks) enter_block(st, k, nblocks);
             // this step's sim vector (lane 0's row just entered; others re-read resident rows)
-            const int4* sim_ring = reinterpret_cast<const int4*>(smem) + lane;          // row stride STRIP/4
             int4* out_ring = reinterpret_cast<int4*>(st.out_gen) + lane;
-            const int* bnd_ring = st.out_gen + OUT_ROWS * STRIP;
-            sv = sim_ring[((k * TILE - lane) & (SIM_ROWS - 1)) * (STRIP / 4)];
+            const uint32_t sim_lane = st.sim_base + 16u * lane;   // + row * STRIP*4
+            // sim vectors run PF steps ahead in a register queue (static indices under
+            // full unrolling); at every block start the queue is refilled because
+            // lane 0's prefetches past the block edge may have read unlanded rows
+            constexpr int PF = 4;
+            int4 svq[PF];
+#pragma unroll
+            for (int d = 0; d < PF; ++d)
+                svq[d] = lds128v(sim_lane + (uint32_t)(((k * TILE + d - lane) & (SIM_ROWS - 1)) * STRIP) * 4u);
+            int bvq[PF];
+#pragma unroll
+            for (int d = 0; d < PF; ++d) bvq[d] = lds32v(st.bnd_base + 4u * ((k * TILE + d) & (BND_RING - 1)));
 #pragma unroll
             for (int u = 0; u < TILE; ++u) {
                 const int s = k * TILE + u;
                 const int i = s - lane;                  // row of this lane (may be < 0 or >= n)
+                const int4 sv = svq[u % PF];
+                const int bv = bvq[u % PF];
+                svq[u % PF] = lds128v(sim_lane + (uint32_t)(((i + PF) & (SIM_ROWS - 1)) * STRIP) * 4u);
+                bvq[u % PF] = lds32v(st.bnd_base + 4u * ((s + PF) & (BND_RING - 1)));
                 // everything not fed by the left neighbour first (overlaps the shuffle):
                 // x_c = max(diag_c + sim_c, up_c - p); the chain is then v_c = max(v_{c-1} - p, x_c)
                 const int x0 = max(left_prev + sv.x, h0 - p);
                 const int x1 = max(h0 + sv.y, h1 - p);
                 const int x2 = max(h1 + sv.z, h2 - p);
                 const int x3 = max(h2 + sv.w, h3 - p);
-                const int bv = bnd_ring[s & (BND_RING - 1)];
                 const int shl = __shfl_up_sync(0xffffffffu, h3, 1);
                 const int left = lane == 0 ? bv : shl;
                 const int v0 = max(left - p, x0);
@@ -236,8 +258,6 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                     left_prev = left;
                 }
                 out_ring[(i & (OUT_ROWS - 1)) * (STRIP / 4)] = make_int4(h0, h1, h2, h3);
-                // next row's sim vector (its block is resident: entered at the block start)
-                sv = sim_ring[((i + 1) & (SIM_ROWS - 1)) * (STRIP / 4)];
             }
         }
         cp_async_wait_all();
