@@ -238,6 +238,52 @@ LEGO_GLOBAL void __launch_bounds__(128) lego_remap(const unsigned char* __restri
         lego_st16(d + (f0 + (long long)y * gen::DY + k * LEGO_V) * LEGO_ELEM, v);
     }
 }
+#elif LEGO_PERSIST
+// Persistent variant: a fixed grid (a few CTAs per SM) whose warps stride
+// over the warp tiles, loading tile t + stride while tile t is transposed and
+// stored -- no CTA launch churn, and every lane always has a tile's worth of
+// 16-byte loads in flight.
+static __device__ __forceinline__ void lego_tile_load(const unsigned char* s, long long t, int xg, int yg,
+                                                      long long& f0, lego_v16 (&rows)[LEGO_V]) {
+    long long s0;
+    gen::origin(t, f0, s0);
+    const unsigned char* sp = s + (s0 + (long long)(xg * LEGO_V) * gen::SX + yg * LEGO_V) * LEGO_ELEM;
+#pragma unroll
+    for (int r = 0; r < LEGO_V; ++r) rows[r] = lego_ld16(sp + (long long)r * gen::SX * LEGO_ELEM);
+}
+static __device__ __forceinline__ void lego_tile_store(unsigned char* d, long long f0, int xg, int yg,
+                                                       const lego_v16 (&rows)[LEGO_V]) {
+    lego_v16 cols[LEGO_V];
+    lego_transpose(rows, cols);
+    unsigned char* dp = d + (f0 + (long long)(yg * LEGO_V) * gen::DY + xg * LEGO_V) * LEGO_ELEM;
+#pragma unroll
+    for (int c = 0; c < LEGO_V; ++c) lego_st16(dp + (long long)c * gen::DY * LEGO_ELEM, cols[c]);
+}
+LEGO_GLOBAL void __launch_bounds__(256, 2) lego_remap(const unsigned char* __restrict__ src,
+                                                      unsigned char* __restrict__ dst,
+                                                      long long src_stride, long long dst_stride) {
+    const int lane = threadIdx.x & 31;
+    const long long stride = (long long)gridDim.x * (blockDim.x >> 5);
+    long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (t >= gen::TILES) return;
+    const unsigned char* s = src + (long long)blockIdx.y * src_stride * LEGO_ELEM;
+    unsigned char* d = dst + (long long)blockIdx.y * dst_stride * LEGO_ELEM;
+    const int yg = lane & 7, xg = lane >> 3;
+    lego_v16 a[LEGO_V], b[LEGO_V];
+    long long fa, fb;
+    lego_tile_load(s, t, xg, yg, fa, a);
+    for (;;) {
+        const long long t1 = t + stride;
+        if (t1 >= gen::TILES) { lego_tile_store(d, fa, xg, yg, a); return; }
+        lego_tile_load(s, t1, xg, yg, fb, b);
+        lego_tile_store(d, fa, xg, yg, a);
+        const long long t2 = t1 + stride;
+        if (t2 >= gen::TILES) { lego_tile_store(d, fb, xg, yg, b); return; }
+        lego_tile_load(s, t2, xg, yg, fa, a);
+        lego_tile_store(d, fb, xg, yg, b);
+        t = t2;
+    }
+}
 #else
 LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
                                                    unsigned char* __restrict__ dst,

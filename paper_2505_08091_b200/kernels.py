@@ -125,6 +125,7 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
     if not masked:
         variant = TRANSPOSE_VARIANT or ("reg" if elem_bytes == 2 else "smem")
         smem_variant = variant == "smem"
+        persist = variant == "persist"
         tpw = 2 if variant == "reg2" else 1
         tp = lower.transpose_plan(g, f, n_dst, elem_bytes, 8 if smem_variant else 4, 8)
         if tp is not None:
@@ -136,11 +137,15 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
             v = 16 // elem_bytes
             smem = warps * 8 * v * 8 * 16 if smem_variant else 0
             per_cta = warps * tpw
+            units = (tp.tiles + per_cta - 1) // per_cta
+            if persist:
+                units = min(units, PERSIST_CTAS)
             info = runtime.ProgramInfo(kind=runtime.KIND_TRANSPOSE, elem_bytes=elem_bytes, n=n_dst,
-                                       units=(tp.tiles + per_cta - 1) // per_cta, unit_threads=32,
-                                       block=32 * warps, smem_bytes=smem)
+                                       units=units, unit_threads=32, block=32 * warps,
+                                       smem_bytes=smem)
             src = _assemble(body, {"LEGO_KIND": 2, "LEGO_ELEM": elem_bytes,
-                                   "LEGO_SMEM": int(smem_variant), "LEGO_TPW": tpw})
+                                   "LEGO_SMEM": int(smem_variant), "LEGO_TPW": tpw,
+                                   "LEGO_PERSIST": int(persist)})
             return RemapPlan(runtime.KIND_TRANSPOSE, n_dst, n_src, elem_bytes, False, False, src,
                              info, f"tile {tp.tx}x{tp.ty} {variant}, SX={tp.sx}, DY={tp.dy}")
     width = 1 if masked else lower.contiguous_width(g, f, n_dst, widths=(vec,))
@@ -165,6 +170,8 @@ BAND_ROWS, BAND_DIAGS = 64, 64
 # through swizzled shared memory); empty = per element size, as measured on
 # B200 (scripts/quick_time.py): reg for 2-byte elements, smem otherwise
 TRANSPOSE_VARIANT = os.environ.get("LEGO_TRANSPOSE", "")
+# CTAs of the persistent transpose variant (2 resident CTAs x 148 SMs by default)
+PERSIST_CTAS = int(os.environ.get("LEGO_PERSIST_CTAS", str(2 * 148)))
 # band tile order: 0 row-block major, 1 diagonal-block major, -1 = per direction
 BAND_ORDER = int(os.environ.get("LEGO_BAND_ORDER", "-1"))
 
@@ -203,7 +210,7 @@ def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
 
 def _remap_program(src_layout, dst_layout, elem_bytes):
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, TRANSPOSE_VARIANT,
-           BAND_ORDER)
+           BAND_ORDER, PERSIST_CTAS)
     plan_box = {}
 
     def build():

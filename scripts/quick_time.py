@@ -23,6 +23,8 @@ def t(fn, iters=30):
 
 
 which = sys.argv[1:] or ["transpose", "band", "nw"]
+if __name__ != "__main__":
+    which = []
 if "transpose" in which:
     g = L.parse_layout("GroupBy([16384,16384]).OrderBy(Col(16384,16384))")
     for dt in (torch.bfloat16, torch.float32, torch.uint8):
