@@ -34,9 +34,10 @@ elif name == "gemm":
     b = torch.randn(8192, 8192, device="cuda").to(torch.bfloat16)
     c = torch.empty(8192, 8192, device="cuda", dtype=torch.bfloat16)
     fn = lambda: K.gemm(a, b, out=c)  # noqa: E731
-elif name == "nw":
-    sim = torch.randint(-10, 11, (16384, 16384), device="cuda", dtype=torch.int32)
-    score = torch.empty(16385, 16385, device="cuda", dtype=torch.int32)
+elif name.startswith("nw"):
+    n = int(name[2:] or 16384)
+    sim = torch.randint(-10, 11, (n, n), device="cuda", dtype=torch.int32)
+    score = torch.empty(n + 1, n + 1, device="cuda", dtype=torch.int32)
     fn = lambda: K.nw_score(sim, 10, out=score)  # noqa: E731
 elif name == "apply_map":
     g = L.parse_layout("GroupBy([16384,16384]).OrderBy(GenP([16384,16384], antidiag))")
