@@ -8,22 +8,20 @@
 //  * the n columns are cut into 128-wide strips, one warp per strip, claimed
 //    in order from an atomic ticket, so a strip's left neighbour is always
 //    already running;
-//  * a strip is two 64-column *chains*; in chain g lane j owns columns
-//    64g + 2j, 64g + 2j + 1 and at warp step s computes row s - 32g - j:
-//    every step advances one anti-diagonal of each chain (the LEGO antidiag
-//    order of the paper's NW kernel).  The left value
-//    arrives by a rotating warp shuffle: lane j reads lane j-1, lane 0 reads
-//    lane 31, which sends chain g-1's last column (computed one step
-//    earlier) or, for chain 0, the left strip's boundary value.  The two
-//    chains are independent within a step, so each one's shuffle latency is
-//    hidden behind the other's work; up and diagonal values are the lane's
-//    own previous row;
+//  * inside a strip the warp sweeps anti-diagonally: lane j owns columns
+//    4j..4j+3 and at step s computes row s - j, i.e. every step is one
+//    anti-diagonal of the (rows x 32 lane-columns) grid -- the LEGO antidiag
+//    order of the paper's NW kernel.  The value from the
+//    left arrives by warp shuffle, the up and diagonal values are the lane's
+//    own previous row: the per-step critical path is one shuffle plus a
+//    4-cell max/add chain, and the step body is branch-free (steps are
+//    grouped 32 at a time so all bookkeeping happens once per block);
 //  * sim is staged 32 rows x 128 columns at a time by cp.async one block
-//    ahead into a 128-row ring and read from shared memory four steps ahead
-//    (register queue); results go to a 128-row ring and leave as coalesced
-//    row segments once a block of rows is complete, when the strip's last
-//    column is also published to a global boundary array with one
-//    st.release (polled by the right neighbour once per 32 rows).
+//    ahead into a 4-block ring, read back one step early along the
+//    anti-diagonal (16-byte, conflict-free); results go to a 2-block ring and
+//    leave as coalesced row segments once a block is complete; the strip's
+//    last column is then published to a global boundary array with one
+//    st.release, which the right neighbour polls once per 32 rows.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -33,15 +31,12 @@
 namespace {
 
 constexpr int TILE = 32;                 // rows per block
-constexpr int CHAINS = 2;                // independent chains per warp
-constexpr int CPL = 2;                   // columns per lane per chain
-constexpr int CHAIN_COLS = 32 * CPL;     // 64
-constexpr int STRIP = CHAINS * CHAIN_COLS;   // 128 columns per warp
-constexpr int RING = 128;                // rows in the sim ring and in the out ring
-constexpr int BND_RING = 64;
-constexpr int LAG = TILE * (CHAINS - 1) + 31;   // steps from chain 0 lane 0 to the last cell of a row
-constexpr int SMEM_BYTES = 2 * RING * STRIP * 4 + BND_RING * 4;
-constexpr int PF = 4;                    // sim prefetch distance (steps)
+constexpr int CPL = 4;                   // columns per lane
+constexpr int STRIP = 32 * CPL;          // columns per warp strip
+constexpr int SIM_ROWS = 4 * TILE;       // sim ring: 4 blocks
+constexpr int OUT_ROWS = 2 * TILE;       // out ring: 2 blocks
+constexpr int BND_RING = 2 * TILE;
+constexpr int SMEM_BYTES = (SIM_ROWS + OUT_ROWS) * STRIP * 4 + BND_RING * 4;
 
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
@@ -60,9 +55,10 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ int2 lds64v(uint32_t a) {
-    int2 v;
-    asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+
+__device__ __forceinline__ int4 lds128v(uint32_t a) {
+    int4 v;
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
 __device__ __forceinline__ int lds32v(uint32_t a) {
@@ -96,13 +92,15 @@ struct Strip {
     int32_t* out_gen;                        // generic pointer of the out ring
 };
 
-// stage sim rows [32k, 32k+32) of the strip into the ring (one cp.async group)
+// stage sim rows [32k, 32k+32) into ring block k % 4 (one cp.async group)
 __device__ __forceinline__ void stage_sim(const Strip& st, int k) {
+    // pointer-walking, fully unrolled: ~3 instructions per row (the issue cost
+    // of this loop competes with the wavefront steps of the same warp)
     const int rows = min(TILE, st.n - k * TILE);
-    uint32_t dst = st.sim_base + (uint32_t)(((k * TILE) & (RING - 1)) * STRIP) * 4u;
+    uint32_t dst = st.sim_base + (uint32_t)((k & 3) * TILE * STRIP) * 4u;
     if (st.vec_ok) {
-        const int32_t* src = st.simb + (long long)k * TILE * st.n + st.col0 + 4 * st.lane;
-        const bool ok = st.col0 + 4 * st.lane < st.n;
+        const int32_t* src = st.simb + (long long)k * TILE * st.n + st.col0 + CPL * st.lane;
+        const bool ok = st.col0 + CPL * st.lane < st.n;
         dst += 16u * st.lane;
 #pragma unroll
         for (int r = 0; r < TILE; ++r) {
@@ -115,7 +113,7 @@ __device__ __forceinline__ void stage_sim(const Strip& st, int k) {
         dst += 4u * st.lane;
         for (int r = 0; r < rows; ++r) {
 #pragma unroll
-            for (int q = 0; q < STRIP / 32; ++q)
+            for (int q = 0; q < CPL; ++q)
                 if (st.col0 + q * 32 + st.lane < st.n) cp_async4(dst + 128u * q, src + 32 * q);
             dst += STRIP * 4u;
             src += st.n;
@@ -124,8 +122,8 @@ __device__ __forceinline__ void stage_sim(const Strip& st, int k) {
     cp_async_commit();
 }
 
-// block k enters (chain 0 lane 0 reaches row 32k): sim block k landed, block
-// k+1 in flight, left boundary rows of block k in the ring
+// block k enters: sim block k landed (block k+1 in flight), boundary rows of
+// block k in the ring (analytic column 0 for the first strip)
 __device__ __forceinline__ void enter_block(const Strip& st, int k, int nblocks) {
     if (k + 1 < nblocks) {
         stage_sim(st, k + 1);
@@ -155,7 +153,7 @@ __device__ __forceinline__ void enter_block(const Strip& st, int k, int nblocks)
 // block k is complete: publish its boundary column, then write its rows out
 __device__ __forceinline__ void flush_block(const Strip& st, int k) {
     __syncwarp();
-    const int32_t* src = st.out_gen + ((k * TILE) & (RING - 1)) * STRIP;
+    const int32_t* src = st.out_gen + (k & 1) * TILE * STRIP;
     const int brow = k * TILE + st.lane;
     if (brow < st.n) st.my_bnd[brow] = src[st.lane * STRIP + STRIP - 1];
     __threadfence();
@@ -165,13 +163,13 @@ __device__ __forceinline__ void flush_block(const Strip& st, int k) {
     const int rows = min(TILE, st.n - k * TILE);
     int32_t* dst = st.sc + (long long)(k * TILE + 1) * ld + st.col0 + 1 + st.lane;
     const int32_t* s = src + st.lane;
-    bool ok[STRIP / 32];
+    bool ok[CPL];
 #pragma unroll
-    for (int q = 0; q < STRIP / 32; ++q) ok[q] = st.col0 + q * 32 + st.lane < st.n;
+    for (int q = 0; q < CPL; ++q) ok[q] = st.col0 + q * 32 + st.lane < st.n;
 #pragma unroll 8
     for (int r = 0; r < rows; ++r) {
 #pragma unroll
-        for (int q = 0; q < STRIP / 32; ++q)
+        for (int q = 0; q < CPL; ++q)
             if (ok[q]) dst[32 * q] = s[32 * q];
         dst += ld;
         s += STRIP;
@@ -192,12 +190,9 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
     st.lane = lane;
     st.vec_ok = (n % 4) == 0;
     st.sim_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    st.out_base = st.sim_base + RING * STRIP * 4;
-    st.bnd_base = st.out_base + RING * STRIP * 4;
-    st.out_gen = smem + RING * STRIP;
-    // per-lane byte offsets of chain g's two columns inside a ring row
-    const uint32_t lane_off0 = 4u * (CPL * lane);
-    const uint32_t lane_off1 = 4u * (CHAIN_COLS + CPL * lane);
+    st.out_base = st.sim_base + SIM_ROWS * STRIP * 4;
+    st.bnd_base = st.out_base + OUT_ROWS * STRIP * 4;
+    st.out_gen = smem + SIM_ROWS * STRIP;
 
     for (;;) {
         int strip = 0;
@@ -213,60 +208,56 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
         st.my_prog = progress + strip;
         st.left_prog = progress + strip - 1;
         st.col0 = st.w * STRIP;
-        // 0-based sim column of the first column this lane owns in chain 0 / chain 1
-        const int c0 = st.col0 + CPL * lane, c1 = c0 + CHAIN_COLS;
+        const int c_lane = st.col0 + CPL * lane;
 
         stage_sim(st, 0);
-        // h: the lane's two cells of the previous row (S[0][c+1], S[0][c+2] to start)
-        int a0 = -(c0 + 1) * p, a1 = -(c0 + 2) * p;       // chain 0
-        int b0 = -(c1 + 1) * p, b1 = -(c1 + 2) * p;       // chain 1
-        int la = -c0 * p, lb = -c1 * p;                    // S[i][c] of the cell left of each chain's lane
+        int32_t h0 = -(c_lane + 1) * p, h1 = -(c_lane + 2) * p, h2 = -(c_lane + 3) * p,
+                h3 = -(c_lane + 4) * p;                    // S[0][c+1..c+4]
+        int32_t left_prev = -c_lane * p;                    // S[0][c_lane]
 
-        // blocks enter while chain 0 needs them; the extra iterations drain chain 1 and the flushes
-        const int last_iter = nblocks + (LAG + TILE - 1) / TILE + 1;
-        for (int k = 0; k <= last_iter; ++k) {
-            if (k >= 3) flush_block(st, k - 3);            // block k-3 completed at step 32k - 2
-            if (k >= last_iter) break;
+        for (int k = 0; k <= nblocks + 1; ++k) {
+            if (k >= 2) flush_block(st, k - 2);
+            if (k > nblocks) break;
             if (k < nblocks) enter_block(st, k, nblocks);
-            // operand queues, PF steps ahead; refilled at every block start because
-            // reads past the entering block may have seen unlanded rows
-            int2 qa[PF], qb[PF];
-            int qbv[PF];
+            // this step's sim vector (lane 0's row just entered; others re-read resident rows)
+            int4* out_ring = reinterpret_cast<int4*>(st.out_gen) + lane;
+            const uint32_t sim_lane = st.sim_base + 16u * lane;   // + row * STRIP*4
+            // sim vectors run PF steps ahead in a register queue (static indices under
+            // full unrolling); at every block start the queue is refilled because
+            // lane 0's prefetches past the block edge may have read unlanded rows
+            constexpr int PF = 4;
+            int4 svq[PF];
 #pragma unroll
-            for (int d = 0; d < PF; ++d) {
-                const int s = k * TILE + d;
-                qa[d] = lds64v(st.sim_base + (uint32_t)(((s - lane) & (RING - 1)) * STRIP) * 4u + lane_off0);
-                qb[d] = lds64v(st.sim_base + (uint32_t)(((s - TILE - lane) & (RING - 1)) * STRIP) * 4u + lane_off1);
-                qbv[d] = lds32v(st.bnd_base + 4u * (s & (BND_RING - 1)));
-            }
+            for (int d = 0; d < PF; ++d)
+                svq[d] = lds128v(sim_lane + (uint32_t)(((k * TILE + d - lane) & (SIM_ROWS - 1)) * STRIP) * 4u);
+            int bvq[PF];
+#pragma unroll
+            for (int d = 0; d < PF; ++d) bvq[d] = lds32v(st.bnd_base + 4u * ((k * TILE + d) & (BND_RING - 1)));
 #pragma unroll
             for (int u = 0; u < TILE; ++u) {
                 const int s = k * TILE + u;
-                const int ia = s - lane;                   // chain 0 row of this lane
-                const int ib = ia - TILE;                  // chain 1 row of this lane
-                const int2 sa = qa[u % PF], sb = qb[u % PF];
-                const int bv = qbv[u % PF];
-                qa[u % PF] = lds64v(st.sim_base + (uint32_t)(((ia + PF) & (RING - 1)) * STRIP) * 4u + lane_off0);
-                qb[u % PF] = lds64v(st.sim_base + (uint32_t)(((ib + PF) & (RING - 1)) * STRIP) * 4u + lane_off1);
-                qbv[u % PF] = lds32v(st.bnd_base + 4u * ((s + PF) & (BND_RING - 1)));
-                // left-independent parts: x_c = max(diag_c + sim_c, up_c - p)
-                const int xa0 = max(la + sa.x, a0 - p), xa1 = max(a0 + sa.y, a1 - p);
-                const int xb0 = max(lb + sb.x, b0 - p), xb1 = max(b0 + sb.y, b1 - p);
-                // rotating shuffle: lane 31 feeds lane 0 -- chain 0 gets the left strip's
-                // boundary, chain 1 gets chain 0's last column of the previous step
-                const int sa_send = lane == 31 ? bv : a1;
-                const int sb_send = lane == 31 ? a1 : b1;
-                const int left_a = __shfl_sync(0xffffffffu, sa_send, (lane + 31) & 31);
-                const int left_b = __shfl_sync(0xffffffffu, sb_send, (lane + 31) & 31);
-                const int va0 = max(left_a - p, xa0), va1 = max(va0 - p, xa1);
-                const int vb0 = max(left_b - p, xb0), vb1 = max(vb0 - p, xb1);
-                if (ia >= 0) { a0 = va0; a1 = va1; la = left_a; }     // lanes start one step apart,
-                if (ib >= 0) { b0 = vb0; b1 = vb1; lb = left_b; }     // chain 1 one block later
-                if ((unsigned)ia < (unsigned)n)
-                    *reinterpret_cast<int2*>(st.out_gen + (ia & (RING - 1)) * STRIP + CPL * lane) = make_int2(a0, a1);
-                if ((unsigned)ib < (unsigned)n)
-                    *reinterpret_cast<int2*>(st.out_gen + (ib & (RING - 1)) * STRIP + CHAIN_COLS + CPL * lane) =
-                        make_int2(b0, b1);
+                const int i = s - lane;                  // row of this lane (may be < 0 or >= n)
+                const int4 sv = svq[u % PF];
+                const int bv = bvq[u % PF];
+                svq[u % PF] = lds128v(sim_lane + (uint32_t)(((i + PF) & (SIM_ROWS - 1)) * STRIP) * 4u);
+                bvq[u % PF] = lds32v(st.bnd_base + 4u * ((s + PF) & (BND_RING - 1)));
+                // everything not fed by the left neighbour first (overlaps the shuffle):
+                // x_c = max(diag_c + sim_c, up_c - p); the chain is then v_c = max(v_{c-1} - p, x_c)
+                const int x0 = max(left_prev + sv.x, h0 - p);
+                const int x1 = max(h0 + sv.y, h1 - p);
+                const int x2 = max(h1 + sv.z, h2 - p);
+                const int x3 = max(h2 + sv.w, h3 - p);
+                const int shl = __shfl_up_sync(0xffffffffu, h3, 1);
+                const int left = lane == 0 ? bv : shl;
+                const int v0 = max(left - p, x0);
+                const int v1 = max(v0 - p, x1);
+                const int v2 = max(v1 - p, x2);
+                const int v3 = max(v2 - p, x3);
+                if (k > 0 || i >= 0) {                   // lanes start one step apart
+                    h0 = v0; h1 = v1; h2 = v2; h3 = v3;
+                    left_prev = left;
+                }
+                out_ring[(i & (OUT_ROWS - 1)) * (STRIP / 4)] = make_int4(h0, h1, h2, h3);
             }
         }
         cp_async_wait_all();
@@ -307,7 +298,8 @@ extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long ctas = total < sms ? total : sms;      // one strip-warp per SM (128 KiB staging)
+    const long long cap = 2LL * sms;       // two strips per SM fit the staging rings
+    const long long ctas = total < cap ? total : cap;
     nw_strips<<<(unsigned)ctas, 32, SMEM_BYTES, st>>>(sim, score, (int)n, penalty, strips, (int)total, ticket,
                                                       progress, bnd);
     lego_status s = lego_cuda_check(cudaGetLastError(), "nw launch");
