@@ -298,7 +298,13 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
     if (t0 >= gen::TILES) return;
     const unsigned char* s = src + (long long)blockIdx.y * src_stride * LEGO_ELEM;
     unsigned char* d = dst + (long long)blockIdx.y * dst_stride * LEGO_ELEM;
+#if LEGO_XMAJOR
+    // 8 lanes along x (128-byte dst runs), 4 along y (64-byte src runs)
+    const int xg = lane & 7, yg = lane >> 3;
+#else
+    // 8 lanes along y (128-byte src runs), 4 along x (64-byte dst runs)
     const int yg = lane & 7, xg = lane >> 3;
+#endif
     long long f0[LEGO_TPW];
     lego_v16 rows[LEGO_TPW][LEGO_V];
 #pragma unroll

@@ -126,8 +126,10 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
         variant = TRANSPOSE_VARIANT or ("reg" if elem_bytes == 2 else "smem")
         smem_variant = variant == "smem"
         persist = variant == "persist"
+        xmajor = variant == "regT"
         tpw = 2 if variant == "reg2" else 1
-        tp = lower.transpose_plan(g, f, n_dst, elem_bytes, 8 if smem_variant else 4, 8)
+        xv, yv = (8, 8) if smem_variant else ((8, 4) if xmajor else (4, 8))
+        tp = lower.transpose_plan(g, f, n_dst, elem_bytes, xv, yv, TILE_ORDER)
         if tp is not None:
             body = codegen.constant("N", n_dst) + codegen.constant("TILES", tp.tiles)
             body += codegen.constant("SX", tp.sx) + codegen.constant("DY", tp.dy)
@@ -145,7 +147,7 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
                                        smem_bytes=smem)
             src = _assemble(body, {"LEGO_KIND": 2, "LEGO_ELEM": elem_bytes,
                                    "LEGO_SMEM": int(smem_variant), "LEGO_TPW": tpw,
-                                   "LEGO_PERSIST": int(persist)})
+                                   "LEGO_PERSIST": int(persist), "LEGO_XMAJOR": int(xmajor)})
             return RemapPlan(runtime.KIND_TRANSPOSE, n_dst, n_src, elem_bytes, False, False, src,
                              info, f"tile {tp.tx}x{tp.ty} {variant}, SX={tp.sx}, DY={tp.dy}")
     width = 1 if masked else lower.contiguous_width(g, f, n_dst, widths=(vec,))
@@ -170,6 +172,8 @@ BAND_ROWS, BAND_DIAGS = 64, 64
 # through swizzled shared memory); empty = per element size, as measured on
 # B200 (scripts/quick_time.py): reg for 2-byte elements, smem otherwise
 TRANSPOSE_VARIANT = os.environ.get("LEGO_TRANSPOSE", "")
+# warp-tile walk order of the transpose ("x", "y" or "block", see lower.transpose_plan)
+TILE_ORDER = os.environ.get("LEGO_TILE_ORDER", "x")
 # CTAs of the persistent transpose variant (2 resident CTAs x 148 SMs by default)
 PERSIST_CTAS = int(os.environ.get("LEGO_PERSIST_CTAS", str(2 * 148)))
 # band tile order: 0 row-block major, 1 diagonal-block major, -1 = per direction
@@ -210,7 +214,7 @@ def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
 
 def _remap_program(src_layout, dst_layout, elem_bytes):
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, TRANSPOSE_VARIANT,
-           BAND_ORDER, PERSIST_CTAS)
+           BAND_ORDER, PERSIST_CTAS, TILE_ORDER)
     plan_box = {}
 
     def build():

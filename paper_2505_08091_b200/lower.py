@@ -232,7 +232,7 @@ class TransposePlan:
 
 
 def transpose_plan(g: Expr, f: Var, n: int, elem_bytes: int, x_vectors: int = 4,
-                   y_vectors: int = 8) -> Optional[TransposePlan]:
+                   y_vectors: int = 8, tile_order: str = "x") -> Optional[TransposePlan]:
     """Warp-tiled transpose geometry for a digit-permutation gather: a warp
     tile is (x_vectors*V) x (y_vectors*V) elements, V = 16 / elem_bytes."""
     if 16 % elem_bytes:
@@ -257,17 +257,40 @@ def transpose_plan(g: Expr, f: Var, n: int, elem_bytes: int, x_vectors: int = 4,
             continue
         if stride % v or lo % v:
             return None
-    # tile index t -> (x_hi fastest, mid, y_hi, hi) -> dst origin f0
+    # tile index t -> tile coordinates -> dst origin f0.  The walk order is a
+    # LEGO layout over the tile grid (x_hi, mid, y_hi, hi):
+    #   "x": x_hi fastest (concurrent warps sweep dst rows),
+    #   "y": y_hi fastest (concurrent warps sweep src rows),
+    #   "block": 8 x 8 tile blocks, x fastest inside a block (both sides local)
     x_hi = x_span // tx
     mid = y_lo // x_span
     y_hi = y_span // ty
     hi = n // (y_lo * y_span)
     tiles = x_hi * mid * y_hi * hi
     t = Var("t", VarRange(0, tiles))
-    c0 = t % x_hi
-    c1 = (t // x_hi) % mid
-    c2 = (t // (x_hi * mid)) % y_hi
-    c3 = t // (x_hi * mid * y_hi)
+    order = tile_order
+    if order == "block" and (x_hi % 8 or y_hi % 8):
+        order = "x"
+    if order == "y":
+        c2 = t % y_hi
+        c0 = (t // y_hi) % x_hi
+        c1 = (t // (y_hi * x_hi)) % mid
+        c3 = t // (y_hi * x_hi * mid)
+    elif order == "block":
+        lx = t % 8
+        ly = (t // 8) % 8
+        gx = (t // 64) % (x_hi // 8)
+        gy = (t // (64 * (x_hi // 8))) % (y_hi // 8)
+        rest = t // (x_hi * y_hi)
+        c0 = gx * 8 + lx
+        c2 = gy * 8 + ly
+        c1 = rest % mid
+        c3 = rest // mid
+    else:
+        c0 = t % x_hi
+        c1 = (t // x_hi) % mid
+        c2 = (t // (x_hi * mid)) % y_hi
+        c3 = t // (x_hi * mid * y_hi)
     f0 = simplify(c0 * tx + c1 * x_span + c2 * (ty * y_lo) + c3 * (y_lo * y_span))
     s0 = simplify(substitute(g, {f.name: f0}))
     return TransposePlan(tiles, sx, y_lo, f0, s0, t, tx, ty)

@@ -13,11 +13,11 @@ g = L.parse_layout("GroupBy([16384,16384]).OrderBy(Col(16384,16384))")
 for dt in (torch.bfloat16, torch.float32):
     src = torch.randint(0, 100, (16384 * 16384,), device="cuda").to(dt)
     out = torch.empty_like(src)
-    for var, ctas in (("reg", 0), ("persist", 148), ("persist", 296), ("persist", 444), ("persist", 592),
-                      ("persist", 888)):
-        K.TRANSPOSE_VARIANT = var
-        K.PERSIST_CTAS = ctas or 296
-        ms = t(lambda: K.remap(src, None, g, out=out))
-        ok = torch.equal(out.view(16384, 16384), src.view(16384, 16384).t())
-        print(f"transpose {str(dt):15s} {var:8s} ctas={ctas:4d} {ms*1e3:8.1f} us "
-              f"{2*src.numel()*src.element_size()/ms/1e6:8.1f} GB/s ok={ok}", flush=True)
+    for var in ("reg", "regT", "smem"):
+        for order in ("x", "y", "block"):
+            K.TRANSPOSE_VARIANT = var
+            K.TILE_ORDER = order
+            ms = t(lambda: K.remap(src, None, g, out=out))
+            ok = torch.equal(out.view(16384, 16384), src.view(16384, 16384).t())
+            print(f"transpose {str(dt):15s} {var:5s} order={order:5s} {ms*1e3:8.1f} us "
+                  f"{2*src.numel()*src.element_size()/ms/1e6:8.1f} GB/s ok={ok}", flush=True)
