@@ -123,7 +123,7 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
         raise UnsupportedNode(f"destination size {n_dst} is not a multiple of {vec} elements "
                               f"({elem_bytes}-byte elements, 16-byte vectors)")
     if not masked:
-        variant = TRANSPOSE_VARIANT or ("reg" if elem_bytes == 2 else "smem")
+        variant = TRANSPOSE_VARIANT or ("smem" if elem_bytes == 1 else "regT")
         smem_variant = variant == "smem"
         persist = variant == "persist"
         xmajor = variant == "regT"
@@ -167,13 +167,16 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
 
 
 BAND_ROWS, BAND_DIAGS = 64, 64
-# transpose kernel variant: "reg" (register micro-tiles, 64-byte store runs),
-# "reg2" (two tiles per warp in flight) or "smem" (128-byte runs on both sides
-# through swizzled shared memory); empty = per element size, as measured on
-# B200 (scripts/quick_time.py): reg for 2-byte elements, smem otherwise
+# transpose kernel variant: "reg" (register micro-tiles, 128-byte src runs,
+# 64-byte dst runs), "regT" (the same with 128-byte dst runs, 64-byte src
+# runs), "reg2" (two tiles per warp in flight), "persist" (persistent,
+# cross-tile prefetch) or "smem" (128-byte runs on both sides through
+# swizzled shared memory); empty = measured best on B200
+# (scripts/quick_transpose.py, profiles/r01_transpose_variants.md): regT,
+# with smem for 1-byte elements
 TRANSPOSE_VARIANT = os.environ.get("LEGO_TRANSPOSE", "")
 # warp-tile walk order of the transpose ("x", "y" or "block", see lower.transpose_plan)
-TILE_ORDER = os.environ.get("LEGO_TILE_ORDER", "x")
+TILE_ORDER = os.environ.get("LEGO_TILE_ORDER", "block")
 # CTAs of the persistent transpose variant (2 resident CTAs x 148 SMs by default)
 PERSIST_CTAS = int(os.environ.get("LEGO_PERSIST_CTAS", str(2 * 148)))
 # band tile order: 0 row-block major, 1 diagonal-block major, -1 = per direction
