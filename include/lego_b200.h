@@ -53,14 +53,19 @@ typedef enum {
     LEGO_PROG_INDEX_MAP = 0,   /* lego_apply_map / lego_inv_map / lego_check_bijective */
     LEGO_PROG_GATHER = 1,      /* remap: dst[f] = src[g(f)], per-element g             */
     LEGO_PROG_TRANSPOSE = 2,   /* remap: digit-permutation, register-tiled transpose   */
-    LEGO_PROG_BAND = 3         /* remap: anti-diagonal band tiles through shared memory */
+    LEGO_PROG_BAND = 3,        /* remap: anti-diagonal band tiles through shared memory */
+    LEGO_PROG_SCATTER = 4      /* remap into an injective layout: dst[apply(x)] = src[x] */
 } lego_program_kind;
+
+/* Program geometry.  Index-map programs: n = logical size, units = physical
+ * size.  Remap programs: n = destination elements per matrix (source
+ * elements for SCATTER), units = CTAs per matrix (grid.x; grid.y = batch). */
 
 typedef struct {
     int32_t kind;          /* lego_program_kind                                  */
     int32_t elem_bytes;    /* remap element size (1, 2, 4, 8, 16); 0 for maps   */
-    int64_t n;             /* elements per matrix (map domain size)             */
-    int64_t units;         /* work units per matrix (vectors, warp tiles, bands) */
+    int64_t n;             /* see above                                         */
+    int64_t units;         /* see above                                         */
     int32_t unit_threads;  /* threads per work unit (1 or 32)                   */
     int32_t block;         /* threads per CTA                                   */
     int32_t smem_bytes;    /* dynamic shared memory per CTA                     */

@@ -451,3 +451,31 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
 #endif
 }
 #endif
+
+// ---------------------------------------------------------------------------
+#if LEGO_KIND == 4
+// scatter: dst[apply(x)] = src[x] for a layout without an inverse (injective
+// mode, reference layout.py:304-311, e.g. broadcast / even-map layouts).
+// Each thread reads one 16-byte source vector (coalesced) and stores its
+// elements at their generated positions; untouched positions keep the
+// caller's initial values.
+#define LEGO_VEC (16 / LEGO_ELEM)
+typedef lego_elem<LEGO_ELEM>::t lego_e;
+
+LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
+                                                   unsigned char* __restrict__ dst,
+                                                   long long src_stride, long long dst_stride) {
+    const unsigned char* s = src + (long long)blockIdx.y * src_stride * LEGO_ELEM;
+    lego_e* d = reinterpret_cast<lego_e*>(dst + (long long)blockIdx.y * dst_stride * LEGO_ELEM);
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= gen::N / LEGO_VEC) return;
+    union { lego_v16 v; lego_e e[LEGO_VEC]; } u;
+    u.v = lego_ld16(s + q * 16);
+#pragma unroll
+    for (int k = 0; k < LEGO_VEC; ++k) {
+        long long p;
+        gen::pos_of(q * LEGO_VEC + k, p);
+        if (p >= 0) d[p] = u.e[k];
+    }
+}
+#endif

@@ -104,7 +104,7 @@ class RemapPlan:
         self.source, self.info, self.detail = source, info, detail
 
     def __repr__(self):
-        names = {1: "gather", 2: "transpose", 3: "band"}
+        names = {1: "gather", 2: "transpose", 3: "band", 4: "scatter"}
         return (f"RemapPlan({names[self.kind]}, n={self.n_dst}, elem={self.elem_bytes}B, "
                 f"{self.detail})")
 
@@ -115,6 +115,9 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
     band = _band_plan(src_layout, dst_layout, elem_bytes)
     if band is not None:
         return band
+    scatter = _scatter_plan(src_layout, dst_layout, elem_bytes)
+    if scatter is not None:
+        return scatter
     f, g, n_dst, n_src = lower.gather_expr(src_layout, dst_layout)
     lo, _hi = lower.value_range(g)
     masked = lo < 0
@@ -215,17 +218,42 @@ def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
                      f"{'scatter' if direction == 0 else 'gather'}")
 
 
+def _scatter_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
+    """Row-major source into an injective-mode layout (no inverse exists):
+    a true scatter, dst[apply(x)] = src[x] (LEGO_KIND 4)."""
+    if src_layout is not None or dst_layout is None:
+        return None
+    if not getattr(lower._group(dst_layout), "injective", False):
+        return None
+    if elem_bytes not in (1, 2, 4, 8):
+        raise UnsupportedNode("scatter supports 1, 2, 4 or 8-byte elements")
+    x, app = lower.apply_map_expr(dst_layout)
+    n_src = lower.logical_size(dst_layout)
+    vec = 16 // elem_bytes
+    if n_src % vec:
+        raise UnsupportedNode(f"source size {n_src} is not a multiple of {vec} elements")
+    n_dst = lower.value_range(app)[1] + 1                   # highest position + 1
+    body = codegen.constant("N", n_src) + codegen.generate("pos_of", [x], {"p": app}).source
+    info = runtime.ProgramInfo(kind=runtime.KIND_SCATTER, elem_bytes=elem_bytes, n=n_src,
+                               units=(n_src // vec + 255) // 256, unit_threads=1, block=256,
+                               smem_bytes=0)
+    src = _assemble(body, {"LEGO_KIND": 4, "LEGO_ELEM": elem_bytes})
+    return RemapPlan(runtime.KIND_SCATTER, n_dst, n_src, elem_bytes, False, False, src, info,
+                     f"scatter into an injective layout, {n_dst} positions")
+
+
 def _remap_program(src_layout, dst_layout, elem_bytes):
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, TRANSPOSE_VARIANT,
            BAND_ORDER, PERSIST_CTAS, TILE_ORDER)
-    plan_box = {}
+    plans = []
 
     def build():
-        plan = plan_remap(src_layout, dst_layout, elem_bytes)
-        plan_box["plan"] = plan
-        return plan.source, plan.info
+        plans.append(plan_remap(src_layout, dst_layout, elem_bytes))
+        return plans[0].source, plans[0].info
 
     prog = _program(key, build)
+    if plans:                      # freshly built: remember the sizes it was planned for
+        prog.n_dst, prog.n_src = plans[0].n_dst, plans[0].n_src
     return prog
 
 
@@ -313,8 +341,9 @@ def remap(src, src_layout=None, dst_layout=None, *, out=None, stream=None):
     if not src.is_cuda:
         raise ShapeMismatch("remap takes a CUDA tensor (no CPU path)")
     elem = src.element_size()
-    f_dst = lower.physical_size(dst_layout) if dst_layout is not None else lower.logical_size(src_layout)
-    n_src = lower.physical_size(src_layout) if src_layout is not None else lower.logical_size(dst_layout)
+    lower.check_pair(src_layout, dst_layout)
+    prog = _remap_program(src_layout, dst_layout, elem)
+    f_dst, n_src = prog.n_dst, prog.n_src
     if src.numel() % n_src:
         raise ShapeMismatch(f"source of {src.numel()} elements is not a batch of layouts of "
                             f"size {n_src}")
@@ -322,8 +351,8 @@ def remap(src, src_layout=None, dst_layout=None, *, out=None, stream=None):
     batch = src.numel() // n_src
     batch_shape = tuple(src.shape[:-1]) if src.dim() and src.shape[-1] == n_src else (batch,)
     if out is None:
-        out = torch.empty(*batch_shape, f_dst, dtype=src.dtype, device=src.device)
-    prog = _remap_program(src_layout, dst_layout, elem)
+        alloc = torch.zeros if prog.info.kind == runtime.KIND_SCATTER else torch.empty
+        out = alloc(*batch_shape, f_dst, dtype=src.dtype, device=src.device)
     st = runtime.stream_handle(stream)
     done = 0
     while done < batch or (batch == 0 and done == 0):

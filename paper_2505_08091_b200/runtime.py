@@ -49,7 +49,7 @@ class ProgramInfo(ctypes.Structure):
                 ("reserved", ctypes.c_int32)]
 
 
-KIND_INDEX_MAP, KIND_GATHER, KIND_TRANSPOSE, KIND_BAND = 0, 1, 2, 3
+KIND_INDEX_MAP, KIND_GATHER, KIND_TRANSPOSE, KIND_BAND, KIND_SCATTER = 0, 1, 2, 3, 4
 
 _lib = None
 _lock = threading.Lock()

@@ -168,3 +168,45 @@ def test_errors_map_to_reference_exceptions():
         K.remap(torch.zeros(100, device="cuda"), None, g)
     with pytest.raises(L.ArityMismatch):
         K.remap(torch.zeros(4096, device="cuda"), L.parse_layout("GroupBy([4096])"), g)
+
+
+def test_injective_layout_scatter():
+    """Injective-mode layouts (no inverse) scatter: dst[apply(x)] = src[x]
+    (reference layout.py:304-311; test_layout.py even-map)."""
+    def even(shape):
+        return L.GenP(shape, L.PermFn(lambda idx: idx[0] * 2, lambda idx: idx[0] * 2), None, name="even")
+
+    g = L.GroupBy([64], orders=(L.OrderBy(even((64,))),), injective=True)
+    src = torch.arange(64, dtype=torch.int32, device="cuda") + 1
+    out = K.remap(src, None, g).cpu().numpy()
+    want = np.zeros(127, dtype=np.int32)
+    want[0::2] = np.arange(64) + 1
+    np.testing.assert_array_equal(out, want)
+    assert K.apply_map(g).cpu().tolist() == [2 * i for i in range(64)]
+
+
+def test_expand_scatter_and_roundtrip():
+    text = "ExpandBy([30,28],[32,32],GroupBy([32,32]).OrderBy(RegP([2,16,2,16],[1,3,2,4])))"
+    g = L.parse_layout(text)
+    spec = O.parse(text)
+    n_log = O.logical_size(spec)
+    host = np.arange(n_log, dtype=np.int32) + 1
+    got = K.remap(torch.from_numpy(host).cuda(), None, g).cpu().numpy()
+    want = O.remap(host, None, spec, dst_size=O.size(spec))
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("dsl", [
+    # multi-stage chains with in-tile GenPs (SURVEY f1), at a few hundred thousand points
+    "GroupBy([512,512]).OrderBy(RegP([16,32,16,32],[1,3,2,4])).OrderBy(RegP([16,16],[2,1]), GenP([32,32], antidiag))",
+    "GroupBy([384,256]).OrderBy(RegP([384,256],[2,1])).OrderBy(RegP([2,128,3,128],[3,1,4,2]))",
+    "TileOrderBy(Col(16,16), Row(32,32))",
+])
+def test_multistage_chains_vs_oracle(dsl):
+    g = L.parse_layout(dsl)
+    spec = O.parse(dsl)
+    assert np.array_equal(K.apply_map(g, dtype=torch.int64).cpu().numpy(), O.apply_range(spec))
+    assert np.array_equal(K.inv_map(g, dtype=torch.int64).cpu().numpy(), O.inv_range(spec))
+    _check_remap(None, spec, None, g, torch.int32, batch=2)
+    _check_remap(spec, None, g, None, torch.int16, batch=1)
+    assert K.check_bijective(g)
