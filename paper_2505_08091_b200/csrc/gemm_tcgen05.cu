@@ -41,7 +41,6 @@ constexpr int NUM_THREADS = 192;
 constexpr int ACC_COLS = BN;                        // fp32 accumulator columns per buffer
 constexpr int TMEM_COLS = 2 * ACC_COLS;             // double buffered: 512 columns
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int GROUP_M = 16;                         // raster group (LEGO GroupBy tile)
 
 // ---- PTX wrappers ---------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -135,20 +134,21 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // lists tiles group by group (G m-blocks), n-blocks inside a group,
 // m fastest; m-block = g*G + m_in.  Falls back to G = MB % G tail groups.
 struct Raster {
-    int mb, nb, per_batch;
+    int mb, nb, per_batch, group;                          // group = G (m-blocks per group)
     __device__ __forceinline__ void coords(int t, int& b, int& m, int& n) const {
         b = t / per_batch;
         int r = t - b * per_batch;
-        const int full = (mb / GROUP_M) * GROUP_M;         // m-blocks in complete groups
-        const int g_tiles = GROUP_M * nb;
-        if (r < (full / GROUP_M) * g_tiles || full == mb) {
+        const int G = group;
+        const int full = (mb / G) * G;                     // m-blocks in complete groups
+        const int g_tiles = G * nb;
+        if (r < (full / G) * g_tiles || full == mb) {
             const int g = r / g_tiles;
             const int rem = r - g * g_tiles;
-            n = rem / GROUP_M;
-            m = g * GROUP_M + (rem - n * GROUP_M);
+            n = rem / G;
+            m = g * G + (rem - n * G);
         } else {                                           // tail group of mb % G m-blocks
             const int tail = mb - full;
-            const int rem = r - (full / GROUP_M) * g_tiles;
+            const int rem = r - (full / G) * g_tiles;
             n = rem / tail;
             m = full + (rem - n * tail);
         }
@@ -172,7 +172,8 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int kblocks = K / BK;
-    Raster ras{M / BM, N / BN, (M / BM) * (N / BN)};
+    // raster_mode: 0 = row-major tile order, G > 0 = LEGO grouped raster with G m-blocks per group
+    Raster ras{M / BM, N / BN, (M / BM) * (N / BN), raster_mode > 0 ? raster_mode : 1};
     const int total_tiles = ras.per_batch * batch;
 
     if (warp == 0 && lane == 0) {

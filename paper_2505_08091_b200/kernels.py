@@ -412,8 +412,16 @@ def nw_score(sim, penalty: int, *, out=None, stream=None):
     return out
 
 
-def gemm(a, b, *, out=None, raster: int = 1, stream=None):
-    """``C = A @ B.T`` for bf16 ``A (..., M, K)`` and ``B (..., N, K)`` on tcgen05."""
+GEMM_RASTER_GROUP = int(os.environ.get("LEGO_GEMM_GROUP", "16"))
+
+
+def gemm(a, b, *, out=None, raster: Optional[int] = None, stream=None):
+    """``C = A @ B.T`` for bf16 ``A (..., M, K)`` and ``B (..., N, K)`` on tcgen05.
+
+    ``raster`` = G selects the LEGO tile raster
+    ``GroupBy([MB/G, NB, G]).OrderBy(Row(MB/G, NB, G))`` (0 = row-major)."""
+    if raster is None:
+        raster = GEMM_RASTER_GROUP
     torch = _torch()
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or not a.is_cuda:
         raise ShapeMismatch("gemm takes CUDA bfloat16 tensors")
