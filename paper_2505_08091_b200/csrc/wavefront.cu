@@ -20,8 +20,10 @@
 //    ahead into a 4-block ring, read back one step early along the
 //    anti-diagonal (16-byte, conflict-free); results go to a 2-block ring and
 //    leave as coalesced row segments once a block is complete; the strip's
-//    last column is then published to a global boundary array with one
-//    st.release, which the right neighbour polls once per 32 rows.
+//    last column is then published as tagged 64-bit words (value | launch
+//    epoch | row) that the right neighbour's lanes poll directly: one L2
+//    round trip per 32 rows both synchronises and delivers the data, with no
+//    flags and no fences.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -38,14 +40,6 @@ constexpr int OUT_ROWS = 2 * TILE;       // out ring: 2 blocks
 constexpr int BND_RING = 2 * TILE;
 constexpr int SMEM_BYTES = (SIM_ROWS + OUT_ROWS) * STRIP * 4 + BND_RING * 4;
 
-__device__ __forceinline__ void st_release(int* p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
 }
@@ -82,10 +76,9 @@ __global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long
 struct Strip {
     const int32_t* simb;
     int32_t* sc;
-    int32_t* my_bnd;
-    const int32_t* left_bnd;
-    int* my_prog;
-    const int* left_prog;
+    int2* my_bnd2;                           // (value, tag) boundary words of this strip
+    const int2* left_bnd2;                   // ... and of the strip to the left
+    unsigned tag;                            // launch epoch << 21 (rows are < 2^20)
     int n, p, w, col0, lane;
     bool vec_ok;
     uint32_t sim_base, out_base, bnd_base;   // shared-window addresses
@@ -134,14 +127,19 @@ __device__ __forceinline__ void enter_block(const Strip& st, int k, int nblocks)
     const int row = k * TILE + st.lane;
     int32_t v;
     if (st.w > 0) {
-        const int need = min((k + 1) * TILE, st.n);
-        if (st.lane == 0) {
-            while (*reinterpret_cast<const volatile int*>(st.left_prog) < need) {
-            }
-            (void)ld_acquire(st.left_prog);
+        // each lane polls its own tagged boundary word: value and tag arrive in one
+        // single-copy-atomic 64-bit store, so one L2 round trip both synchronises
+        // and delivers the data (no flag, no fences)
+        v = 0;
+        if (row < st.n) {
+            const unsigned want = st.tag | (unsigned)(row + 1);
+            unsigned long long w;
+            do {   // one naturally aligned 64-bit load: single-copy atomic with the store
+                asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(st.left_bnd2 + row)
+                             : "memory");
+            } while ((unsigned)(w >> 32) != want);
+            v = (int)(unsigned)w;
         }
-        __syncwarp();
-        v = row < st.n ? __ldcg(st.left_bnd + row) : 0;
     } else {
         v = -(row + 1) * st.p;               // S[row+1][0]
     }
@@ -155,10 +153,12 @@ __device__ __forceinline__ void flush_block(const Strip& st, int k) {
     __syncwarp();
     const int32_t* src = st.out_gen + (k & 1) * TILE * STRIP;
     const int brow = k * TILE + st.lane;
-    if (brow < st.n) st.my_bnd[brow] = src[st.lane * STRIP + STRIP - 1];
-    __threadfence();
-    __syncwarp();
-    if (st.lane == 0) st_release(st.my_prog, min((k + 1) * TILE, st.n));
+    if (brow < st.n) {
+        const int val = src[st.lane * STRIP + STRIP - 1];
+        const unsigned long long tagged =
+            ((unsigned long long)(st.tag | (unsigned)(brow + 1)) << 32) | (unsigned)val;
+        asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" :: "l"(st.my_bnd2 + brow), "l"(tagged) : "memory");
+    }
     const long long ld = (long long)st.n + 1;
     const int rows = min(TILE, st.n - k * TILE);
     int32_t* dst = st.sc + (long long)(k * TILE + 1) * ld + st.col0 + 1 + st.lane;
@@ -179,7 +179,7 @@ __device__ __forceinline__ void flush_block(const Strip& st, int k) {
 
 __global__ void __launch_bounds__(32)
 nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, int p, int strips_per_matrix,
-          int total_strips, int* __restrict__ ticket, int* __restrict__ progress, int32_t* __restrict__ bnd) {
+          int total_strips, int* __restrict__ ticket, int2* __restrict__ bnd2, unsigned epoch) {
     extern __shared__ __align__(16) int32_t smem[];
     const int lane = threadIdx.x;
     const int n_pad = (n + TILE - 1) / TILE * TILE;
@@ -188,6 +188,7 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
     st.n = n;
     st.p = p;
     st.lane = lane;
+    st.tag = (epoch & 0x7FFu) << 21;
     st.vec_ok = (n % 4) == 0;
     st.sim_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     st.out_base = st.sim_base + SIM_ROWS * STRIP * 4;
@@ -203,10 +204,8 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
         st.w = strip - b * strips_per_matrix;
         st.simb = sim + (long long)b * n * n;
         st.sc = score + (long long)b * ((long long)n + 1) * ((long long)n + 1);
-        st.my_bnd = bnd + (long long)strip * n_pad;
-        st.left_bnd = st.my_bnd - n_pad;
-        st.my_prog = progress + strip;
-        st.left_prog = progress + strip - 1;
+        st.my_bnd2 = bnd2 + (long long)strip * n_pad;
+        st.left_bnd2 = st.my_bnd2 - n_pad;
         st.col0 = st.w * STRIP;
         const int c_lane = st.col0 + CPL * lane;
 
@@ -283,15 +282,17 @@ extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n
     const long long total = (long long)strips * batch;
     if (total > INT32_MAX) return lego_fail(LEGO_E_SHAPE, "NW batch too large");
     const int n_pad = (int)((n + TILE - 1) / TILE * TILE);
-    const size_t prog_bytes = sizeof(int) * (size_t)(total + 1);
-    const size_t bnd_off = (prog_bytes + 255) / 256 * 256;
-    const size_t bnd_bytes = sizeof(int32_t) * (size_t)total * n_pad;
+    const size_t bnd_off = 256;
+    const size_t bnd_bytes = sizeof(int2) * (size_t)total * n_pad;
     char* scratch = nullptr;
     LEGO_TRY(lego_cuda_check(cudaMallocAsync((void**)&scratch, bnd_off + bnd_bytes, st), "cudaMallocAsync"));
-    LEGO_TRY(lego_cuda_check(cudaMemsetAsync(scratch, 0, prog_bytes, st), "cudaMemsetAsync"));
+    // ticket + tagged boundary words start at zero; tags also carry a launch epoch
+    LEGO_TRY(lego_cuda_check(cudaMemsetAsync(scratch, 0, bnd_off + bnd_bytes, st), "cudaMemsetAsync"));
     int* ticket = reinterpret_cast<int*>(scratch);
-    int* progress = ticket + 1;
-    int32_t* bnd = reinterpret_cast<int32_t*>(scratch + bnd_off);
+    int2* bnd2 = reinterpret_cast<int2*>(scratch + bnd_off);
+    static unsigned epoch = 0;
+    epoch = (epoch + 1) & 0x7FFu;
+    if (epoch == 0) epoch = 1;
     static cudaError_t attr = cudaFuncSetAttribute(nw_strips, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    SMEM_BYTES);
     LEGO_TRY(lego_cuda_check(attr, "cudaFuncSetAttribute(nw)"));
@@ -301,7 +302,7 @@ extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n
     const long long cap = 2LL * sms;       // two strips per SM fit the staging rings
     const long long ctas = total < cap ? total : cap;
     nw_strips<<<(unsigned)ctas, 32, SMEM_BYTES, st>>>(sim, score, (int)n, penalty, strips, (int)total, ticket,
-                                                      progress, bnd);
+                                                      bnd2, epoch);
     lego_status s = lego_cuda_check(cudaGetLastError(), "nw launch");
     cudaFreeAsync(scratch, st);
     return s;
