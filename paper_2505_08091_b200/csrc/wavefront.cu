@@ -8,14 +8,15 @@
 //  * the n columns are cut into 128-wide strips, one warp per strip, claimed
 //    in order from an atomic ticket, so a strip's left neighbour is always
 //    already running;
-//  * inside a strip the warp sweeps anti-diagonally: lane j owns columns
-//    4j..4j+3 and at step s computes row s - j, i.e. every step is one
-//    anti-diagonal of the (rows x 32 lane-columns) grid -- the LEGO antidiag
-//    order of the paper's NW kernel.  The value from the
-//    left arrives by warp shuffle, the up and diagonal values are the lane's
-//    own previous row: the per-step critical path is one shuffle plus a
-//    4-cell max/add chain, and the step body is branch-free (steps are
-//    grouped 32 at a time so all bookkeeping happens once per block);
+//  * inside a strip the warp sweeps anti-diagonally over 2x4 cell blocks:
+//    lane j owns columns 4j..4j+3 and at step s computes rows 2(s-j) and
+//    2(s-j)+1, i.e. every step is one anti-diagonal of the (row pairs x 32
+//    lane-columns) grid -- the LEGO antidiag order of the paper's NW kernel
+//    (PAPER.md:1298-1301).  The two left values arrive by warp shuffle, the
+//    up and diagonal values are the lane's own previous rows: the per-step
+//    critical path is one shuffle plus a 5-cell max/add chain for 8 cells,
+//    and the step body is branch-free (steps are grouped 16 at a time so all
+//    bookkeeping happens once per 32-row block);
 //  * sim is staged 32 rows x 128 columns at a time by cp.async one block
 //    ahead into a 4-block ring, read back one step early along the
 //    anti-diagonal (16-byte, conflict-free); results go to a 2-block ring and
@@ -36,7 +37,8 @@ constexpr int TILE = 32;                 // rows per block
 constexpr int CPL = 4;                   // columns per lane
 constexpr int STRIP = 32 * CPL;          // columns per warp strip
 constexpr int SIM_ROWS = 4 * TILE;       // sim ring: 4 blocks
-constexpr int OUT_ROWS = 2 * TILE;       // out ring: 2 blocks
+constexpr int OUT_ROWS = 4 * TILE;       // out ring: 4 blocks (flushed three blocks late)
+constexpr int RPS = 2;                   // rows per lane per step
 constexpr int BND_RING = 2 * TILE;
 constexpr int SMEM_BYTES = (SIM_ROWS + OUT_ROWS) * STRIP * 4 + BND_RING * 4;
 
@@ -151,7 +153,7 @@ __device__ __forceinline__ void enter_block(const Strip& st, int k, int nblocks)
 // block k is complete: publish its boundary column, then write its rows out
 __device__ __forceinline__ void flush_block(const Strip& st, int k) {
     __syncwarp();
-    const int32_t* src = st.out_gen + (k & 1) * TILE * STRIP;
+    const int32_t* src = st.out_gen + ((k * TILE) & (OUT_ROWS - 1)) * STRIP;
     const int brow = k * TILE + st.lane;
     if (brow < st.n) {
         const int val = src[st.lane * STRIP + STRIP - 1];
@@ -210,53 +212,71 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
         const int c_lane = st.col0 + CPL * lane;
 
         stage_sim(st, 0);
+        // h: the lane's 4 cells of the last finished row (S[0][c+1..c+4] to start);
+        // t3: the last cell of the row before it (sent to the right with h3)
         int32_t h0 = -(c_lane + 1) * p, h1 = -(c_lane + 2) * p, h2 = -(c_lane + 3) * p,
-                h3 = -(c_lane + 4) * p;                    // S[0][c+1..c+4]
-        int32_t left_prev = -c_lane * p;                    // S[0][c_lane]
+                h3 = -(c_lane + 4) * p, t3 = 0;
+        int32_t left_prev = -c_lane * p;                    // S[i][c_lane] of the last finished row i
 
-        for (int k = 0; k <= nblocks + 1; ++k) {
-            if (k >= 2) flush_block(st, k - 2);
-            if (k > nblocks) break;
+        // a block of 32 rows is 16 steps for lane 0 (two rows per step); lane 31 runs
+        // 31 steps behind, so block k completes at step 16k + 46 and is flushed at
+        // the start of block k + 3
+        for (int k = 0; k <= nblocks + 2; ++k) {
+            if (k >= 3) flush_block(st, k - 3);
+            if (k > nblocks + 1) break;
             if (k < nblocks) enter_block(st, k, nblocks);
-            // this step's sim vector (lane 0's row just entered; others re-read resident rows)
             int4* out_ring = reinterpret_cast<int4*>(st.out_gen) + lane;
             const uint32_t sim_lane = st.sim_base + 16u * lane;   // + row * STRIP*4
-            // sim vectors run PF steps ahead in a register queue (static indices under
-            // full unrolling); at every block start the queue is refilled because
-            // lane 0's prefetches past the block edge may have read unlanded rows
-            constexpr int PF = 4;
-            int4 svq[PF];
+            // sim rows run PF steps ahead in a register queue (static indices under full
+            // unrolling); refilled at every block start because lane 0's prefetches past
+            // the block edge may have read unlanded rows
+            constexpr int PF = 2;
+            int4 sq0[PF], sq1[PF];
+            int bq0[PF], bq1[PF];
 #pragma unroll
-            for (int d = 0; d < PF; ++d)
-                svq[d] = lds128v(sim_lane + (uint32_t)(((k * TILE + d - lane) & (SIM_ROWS - 1)) * STRIP) * 4u);
-            int bvq[PF];
+            for (int d = 0; d < PF; ++d) {
+                const int s = k * (TILE / RPS) + d;
+                const int r = RPS * (s - lane);
+                sq0[d] = lds128v(sim_lane + (uint32_t)((r & (SIM_ROWS - 1)) * STRIP) * 4u);
+                sq1[d] = lds128v(sim_lane + (uint32_t)(((r + 1) & (SIM_ROWS - 1)) * STRIP) * 4u);
+                bq0[d] = lds32v(st.bnd_base + 4u * ((RPS * s) & (BND_RING - 1)));
+                bq1[d] = lds32v(st.bnd_base + 4u * ((RPS * s + 1) & (BND_RING - 1)));
+            }
 #pragma unroll
-            for (int d = 0; d < PF; ++d) bvq[d] = lds32v(st.bnd_base + 4u * ((k * TILE + d) & (BND_RING - 1)));
-#pragma unroll
-            for (int u = 0; u < TILE; ++u) {
-                const int s = k * TILE + u;
-                const int i = s - lane;                  // row of this lane (may be < 0 or >= n)
-                const int4 sv = svq[u % PF];
-                const int bv = bvq[u % PF];
-                svq[u % PF] = lds128v(sim_lane + (uint32_t)(((i + PF) & (SIM_ROWS - 1)) * STRIP) * 4u);
-                bvq[u % PF] = lds32v(st.bnd_base + 4u * ((s + PF) & (BND_RING - 1)));
-                // everything not fed by the left neighbour first (overlaps the shuffle):
-                // x_c = max(diag_c + sim_c, up_c - p); the chain is then v_c = max(v_{c-1} - p, x_c)
-                const int x0 = max(left_prev + sv.x, h0 - p);
-                const int x1 = max(h0 + sv.y, h1 - p);
-                const int x2 = max(h1 + sv.z, h2 - p);
-                const int x3 = max(h2 + sv.w, h3 - p);
-                const int shl = __shfl_up_sync(0xffffffffu, h3, 1);
-                const int left = lane == 0 ? bv : shl;
-                const int v0 = max(left - p, x0);
+            for (int u = 0; u < TILE / RPS; ++u) {
+                const int s = k * (TILE / RPS) + u;
+                const int r0 = RPS * (s - lane);         // this lane's two rows r0, r0 + 1
+                const int4 a = sq0[u % PF], c = sq1[u % PF];
+                const int b0 = bq0[u % PF], b1 = bq1[u % PF];
+                sq0[u % PF] = lds128v(sim_lane + (uint32_t)(((r0 + RPS * PF) & (SIM_ROWS - 1)) * STRIP) * 4u);
+                sq1[u % PF] = lds128v(sim_lane + (uint32_t)(((r0 + RPS * PF + 1) & (SIM_ROWS - 1)) * STRIP) * 4u);
+                bq0[u % PF] = lds32v(st.bnd_base + 4u * ((RPS * (s + PF)) & (BND_RING - 1)));
+                bq1[u % PF] = lds32v(st.bnd_base + 4u * ((RPS * (s + PF) + 1) & (BND_RING - 1)));
+                // row r0: left-independent parts first (overlap the shuffles)
+                const int x0 = max(left_prev + a.x, h0 - p);
+                const int x1 = max(h0 + a.y, h1 - p);
+                const int x2 = max(h1 + a.z, h2 - p);
+                const int x3 = max(h2 + a.w, h3 - p);
+                // lane j-1 finished rows r0, r0 + 1 in the previous step
+                const int sl0 = __shfl_up_sync(0xffffffffu, t3, 1);
+                const int sl1 = __shfl_up_sync(0xffffffffu, h3, 1);
+                const int left0 = lane == 0 ? b0 : sl0;
+                const int left1 = lane == 0 ? b1 : sl1;
+                const int v0 = max(left0 - p, x0);
                 const int v1 = max(v0 - p, x1);
                 const int v2 = max(v1 - p, x2);
                 const int v3 = max(v2 - p, x3);
-                if (k > 0 || i >= 0) {                   // lanes start one step apart
-                    h0 = v0; h1 = v1; h2 = v2; h3 = v3;
-                    left_prev = left;
+                // row r0 + 1: up = row r0, diagonal of its first cell = row r0's left value
+                const int w0 = max(max(left0 + c.x, v0 - p), left1 - p);
+                const int w1 = max(max(v0 + c.y, v1 - p), w0 - p);
+                const int w2 = max(max(v1 + c.z, v2 - p), w1 - p);
+                const int w3 = max(max(v2 + c.w, v3 - p), w2 - p);
+                if (k > 0 || r0 >= 0) {                  // lanes start one step apart
+                    out_ring[(r0 & (OUT_ROWS - 1)) * (STRIP / 4)] = make_int4(v0, v1, v2, v3);
+                    out_ring[((r0 + 1) & (OUT_ROWS - 1)) * (STRIP / 4)] = make_int4(w0, w1, w2, w3);
+                    h0 = w0; h1 = w1; h2 = w2; h3 = w3; t3 = v3;
+                    left_prev = left1;
                 }
-                out_ring[(i & (OUT_ROWS - 1)) * (STRIP / 4)] = make_int4(h0, h1, h2, h3);
             }
         }
         cp_async_wait_all();
