@@ -117,8 +117,7 @@ __device__ __forceinline__ void stage_sim(const Strip& st, int k) {
     cp_async_commit();
 }
 
-// block k enters: sim block k landed (block k+1 in flight), boundary rows of
-// block k in the ring (analytic column 0 for the first strip)
+// block k enters: sim block k landed, block k+1 in flight
 __device__ __forceinline__ void enter_block(const Strip& st, int k, int nblocks) {
     if (k + 1 < nblocks) {
         stage_sim(st, k + 1);
@@ -126,41 +125,50 @@ __device__ __forceinline__ void enter_block(const Strip& st, int k, int nblocks)
     } else {
         cp_async_wait_all();
     }
-    const int row = k * TILE + st.lane;
-    int32_t v;
-    if (st.w > 0) {
-        // each lane polls its own tagged boundary word: value and tag arrive in one
-        // single-copy-atomic 64-bit store, so one L2 round trip both synchronises
-        // and delivers the data (no flag, no fences)
-        v = 0;
-        if (row < st.n) {
-            const unsigned want = st.tag | (unsigned)(row + 1);
-            unsigned long long w;
-            do {   // one naturally aligned 64-bit load: single-copy atomic with the store
-                asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(st.left_bnd2 + row)
-                             : "memory");
-            } while ((unsigned)(w >> 32) != want);
-            v = (int)(unsigned)w;
-        }
-    } else {
-        v = -(row + 1) * st.p;               // S[row+1][0]
-    }
-    asm volatile("st.shared.b32 [%0], %1;" :: "r"(st.bnd_base + 4u * (row & (BND_RING - 1))), "r"(v)
-                 : "memory");
     __syncwarp();
 }
 
-// block k is complete: publish its boundary column, then write its rows out
+// Left-boundary batches of BATCH rows.  Lanes 0..BATCH-1 load their row's
+// tagged word early (bnd_issue) and check it one batch later (bnd_commit),
+// spinning only if the left strip has not published it yet; the value then
+// goes to the shared ring that lane 0 reads.  Value and tag arrive in one
+// naturally aligned 64-bit store, so one L2 round trip both synchronises and
+// delivers the data.
+constexpr int BATCH = 8;
+
+__device__ __forceinline__ unsigned long long ld_tagged(const int2* p) {
+    unsigned long long w;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return w;
+}
+
+__device__ __forceinline__ unsigned long long bnd_issue(const Strip& st, int batch) {
+    const int row = batch * BATCH + st.lane;
+    if (st.w == 0 || st.lane >= BATCH || row >= st.n) return 0;
+    return ld_tagged(st.left_bnd2 + row);
+}
+
+__device__ __forceinline__ void bnd_commit(const Strip& st, int batch, unsigned long long w) {
+    const int row = batch * BATCH + st.lane;
+    if (st.lane < BATCH) {
+        int v = 0;
+        if (st.w == 0) {
+            v = -(row + 1) * st.p;               // S[row+1][0]
+        } else if (row < st.n) {
+            const unsigned want = st.tag | (unsigned)(row + 1);
+            while ((unsigned)(w >> 32) != want) w = ld_tagged(st.left_bnd2 + row);
+            v = (int)(unsigned)w;
+        }
+        asm volatile("st.shared.b32 [%0], %1;" :: "r"(st.bnd_base + 4u * (row & (BND_RING - 1))), "r"(v)
+                     : "memory");
+    }
+    __syncwarp();
+}
+
+// block k is complete: write its rows out as coalesced row segments
 __device__ __forceinline__ void flush_block(const Strip& st, int k) {
     __syncwarp();
     const int32_t* src = st.out_gen + ((k * TILE) & (OUT_ROWS - 1)) * STRIP;
-    const int brow = k * TILE + st.lane;
-    if (brow < st.n) {
-        const int val = src[st.lane * STRIP + STRIP - 1];
-        const unsigned long long tagged =
-            ((unsigned long long)(st.tag | (unsigned)(brow + 1)) << 32) | (unsigned)val;
-        asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" :: "l"(st.my_bnd2 + brow), "l"(tagged) : "memory");
-    }
     const long long ld = (long long)st.n + 1;
     const int rows = min(TILE, st.n - k * TILE);
     int32_t* dst = st.sc + (long long)(k * TILE + 1) * ld + st.col0 + 1 + st.lane;
@@ -218,6 +226,11 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                 h3 = -(c_lane + 4) * p, t3 = 0;
         int32_t left_prev = -c_lane * p;                    // S[i][c_lane] of the last finished row i
 
+        // boundary batches: 0 committed now, 1 in flight (committed at step 0)
+        bnd_commit(st, 0, bnd_issue(st, 0));
+        unsigned long long bnd_pending = bnd_issue(st, 1);
+        const int nbatches = (n + BATCH - 1) / BATCH;
+
         // a block of 32 rows is 16 steps for lane 0 (two rows per step); lane 31 runs
         // 31 steps behind, so block k completes at step 16k + 46 and is flushed at
         // the start of block k + 3
@@ -246,6 +259,12 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
             for (int u = 0; u < TILE / RPS; ++u) {
                 const int s = k * (TILE / RPS) + u;
                 const int r0 = RPS * (s - lane);         // this lane's two rows r0, r0 + 1
+                if (u % (BATCH / RPS) == 0) {
+                    // lane 0 needs batch b = s / 4 from step 4b; commit b + 1 now, issue b + 2
+                    const int b = s / (BATCH / RPS);
+                    if (b + 1 < nbatches) bnd_commit(st, b + 1, bnd_pending);
+                    bnd_pending = b + 2 < nbatches ? bnd_issue(st, b + 2) : 0;
+                }
                 const int4 a = sq0[u % PF], c = sq1[u % PF];
                 const int b0 = bq0[u % PF], b1 = bq1[u % PF];
                 sq0[u % PF] = lds128v(sim_lane + (uint32_t)(((r0 + RPS * PF) & (SIM_ROWS - 1)) * STRIP) * 4u);
@@ -271,11 +290,25 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                 const int w1 = max(max(v0 + c.y, v1 - p), w0 - p);
                 const int w2 = max(max(v1 + c.z, v2 - p), w1 - p);
                 const int w3 = max(max(v2 + c.w, v3 - p), w2 - p);
-                if (k > 0 || r0 >= 0) {                  // lanes start one step apart
+                if (k > 1 || r0 >= 0) {                  // lanes start one step apart (the
+                    // 31-step skew spans the first two 16-step blocks)
                     out_ring[(r0 & (OUT_ROWS - 1)) * (STRIP / 4)] = make_int4(v0, v1, v2, v3);
                     out_ring[((r0 + 1) & (OUT_ROWS - 1)) * (STRIP / 4)] = make_int4(w0, w1, w2, w3);
                     h0 = w0; h1 = w1; h2 = w2; h3 = w3; t3 = v3;
                     left_prev = left1;
+                    // the strip's last column goes straight to the right neighbour
+                    if (lane == 31 && r0 < n) {
+                        const unsigned long long e0 =
+                            ((unsigned long long)(st.tag | (unsigned)(r0 + 1)) << 32) | (unsigned)v3;
+                        asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" :: "l"(st.my_bnd2 + r0), "l"(e0)
+                                     : "memory");
+                        if (r0 + 1 < n) {
+                            const unsigned long long e1 =
+                                ((unsigned long long)(st.tag | (unsigned)(r0 + 2)) << 32) | (unsigned)w3;
+                            asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" :: "l"(st.my_bnd2 + r0 + 1),
+                                         "l"(e1) : "memory");
+                        }
+                    }
                 }
             }
         }
