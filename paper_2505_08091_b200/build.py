@@ -49,7 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         path = os.path.join(CSRC, src)
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-Xptxas", "-v" if verbose else "-O3", "-c", path, "-o", obj]
+               "-Xptxas", "-v" if verbose else "-O3", *os.environ.get("LEGO_NVCC_FLAGS", "").split(),
+               "-c", path, "-o", obj]
         subprocess.check_call(cmd)
         objs.append(obj)
     tmp = LIB + ".tmp"

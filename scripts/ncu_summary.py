@@ -48,7 +48,11 @@ lines = [f"# ncu summaries ({TAG})", "",
          "on `scripts/one_kernel.py <name>` (one B200, cold-ish cache, serialised; compare shares and",
          "traffic, not absolute times).  Algorithmic bytes = each input element read once + each",
          "output element written once.", ""]
-traffic = {}
+try:
+    with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+        traffic = json.load(fh)
+except (OSError, ValueError):
+    traffic = {}
 for name in ["transpose", "gather", "band", "softmax", "gemm", "nw", "apply_map"]:
     rep = os.path.join(SRC, f"prof_{name}.ncu-rep")
     if not os.path.exists(rep):
