@@ -27,9 +27,9 @@
 //              block, into an 8-block ring (the compute warp overwrites each
 //              sim row with its S' row in place);
 //      warp 2  boundary: polls the left strip's published last column
-//              (tagged 64-bit words in global memory: value | launch epoch |
-//              row) and deposits it, tagged with the row, in a shared ring
-//              that compute lane 0 reads one step ahead;
+//              (32-bit words in global memory, preset to a sentinel no
+//              offset score can take) and hands it in row order, through a
+//              shared ring and a row counter, to compute lane 0;
 //      warp 3  flusher:  converts finished blocks S' -> S and writes them
 //              out as coalesced row segments;
 //  * roles synchronise through monotonic block counters in shared memory
@@ -51,18 +51,27 @@ namespace {
 constexpr int CPL = 4;                               // columns per lane
 constexpr int STRIP = 32 * CPL;                      // columns per strip
 constexpr int BLK = 32;                              // rows per block
-constexpr int STEPS = BLK / 2;                       // compute steps per block
-constexpr int NSLOT = 8;                             // ring blocks
-constexpr int RING_ROWS = NSLOT * BLK;               // 256
+#ifndef NW_RPS
+#define NW_RPS 4                                     // rows per lane per step
+#endif
+constexpr int RPS = NW_RPS;
+constexpr int STEPS = BLK / RPS;                     // compute steps per block
+constexpr int BLAG = (31 + STEPS - 1) / STEPS + 1;   // lane 31 completes block k before block k+BLAG starts
+constexpr int DRAIN = (31 + STEPS - 1) / STEPS;      // extra blocks cover lane 31's 31-step lag
+constexpr int GRP = 8 / RPS;                         // boundary readiness checked every GRP steps
+constexpr int NSLOT = 12;                            // ring blocks
+constexpr int RING_ROWS = NSLOT * BLK;               // 384
+constexpr int BND_ROWS = 256;                        // boundary ring (rows)
+constexpr int BND_GROUPS = BND_ROWS / BLK;
 constexpr int ROW_BYTES = STRIP * 4;                 // 512
 constexpr int RING_BYTES = RING_ROWS * ROW_BYTES;    // 128 KiB
-constexpr int BND_BYTES = RING_ROWS * 4;
+constexpr int BND_BYTES = BND_ROWS * 4;
+constexpr int MBAR_BYTES = NSLOT * 8;
 constexpr int CTRL_BYTES = 64;
-constexpr int SMEM_BYTES = RING_BYTES + BND_BYTES + CTRL_BYTES;
+constexpr int SMEM_BYTES = RING_BYTES + BND_BYTES + MBAR_BYTES + CTRL_BYTES;
 #ifndef NW_POLL_NS
 #define NW_POLL_NS 32                                // boundary poll back-off
 #endif
-constexpr int DRAIN = 2;                             // 32 extra steps cover lane 31's 31-step lag
 
 #ifdef LEGO_NW_DEBUG
 // progress probes written to mapped host memory (readable while the kernel runs):
@@ -76,11 +85,13 @@ __device__ __forceinline__ unsigned nw_now() {
     asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(t));
     return t;
 }
+__device__ __forceinline__ void g_nw_trace_strip(int strip) { g_nw_trace[(blockIdx.x * 4 + 3) * 2048 + 2047] = strip + 1; }
 #define NW_TRACE(role, idx) \
     do { if ((idx) < 2048) g_nw_trace[(blockIdx.x * 4 + (role)) * 2048 + (idx)] = nw_now(); } while (0)
 #else
 #define NW_PROBE(v) ((void)0)
 #define NW_TRACE(role, idx) ((void)0)
+#define g_nw_trace_strip(s) ((void)0)
 #endif
 
 struct Ctrl {
@@ -122,13 +133,12 @@ __device__ __forceinline__ void sts128(uint32_t a, int x, int y, int z, int w) {
 __device__ __forceinline__ void sts64(uint32_t a, unsigned long long v) {
     asm volatile("st.shared.b64 [%0], %1;" :: "r"(a), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long* p) {
-    unsigned long long w;
-    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+// boundary words start as NW_EMPTY (|S'| < 2^30 never equals it)
+constexpr int NW_EMPTY = (int)0x80808080;
+__device__ __forceinline__ int ld_bnd(const int* p) {
+    int w;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(w) : "l"(p) : "memory");
     return w;
-}
-__device__ __forceinline__ void st_tagged(unsigned long long* p, unsigned long long w) {
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" :: "l"(p), "l"(w) : "memory");
 }
 
 __global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long long batch) {
@@ -144,103 +154,134 @@ __global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long
 }
 
 // compute-warp state: S' of the lane's 4 columns in its last finished row,
-// the diagonal predecessor of its first column, and the two values it sends
+// the diagonal predecessor of its first column, the last-column values it
+// sends right, and sim rows prefetched two steps ahead
 struct Lane {
-    int h0, h1, h2, h3, dprev, vs3, ws3;
+    int h[CPL];
+    int dprev;
+    int send[RPS];
+    int4 nx1[RPS], nx2[RPS];
+    int bv[RPS];
 };
 
-__device__ __forceinline__ int2 lds64v(uint32_t a) {
-    int2 v;
-    asm volatile("ld.volatile.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-    return v;
+template <int N>
+__device__ __forceinline__ void ldsv(uint32_t a, int (&v)[N]);
+template <>
+__device__ __forceinline__ void ldsv<2>(uint32_t a, int (&v)[2]) {
+    asm volatile("ld.volatile.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(a));
+}
+template <>
+__device__ __forceinline__ void ldsv<4>(uint32_t a, int (&v)[4]) {
+    asm volatile("ld.volatile.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(a));
 }
 
-// predicated (branch-free) publication of two tagged boundary words
-__device__ __forceinline__ void publish2(unsigned long long* p, int pred, int v0, unsigned t0, int v1, unsigned t1) {
+// predicated (branch-free) publication of RPS consecutive boundary words
+__device__ __forceinline__ void publish(int* p, int pred, const int (&v)[RPS]) {
+#if NW_RPS == 4
     asm volatile(
-        "{\n\t.reg .pred q;\n\t.reg .b64 a, b;\n\t"
-        "setp.ne.s32 q, %1, 0;\n\t"
-        "mov.b64 a, {%2, %3};\n\t"
-        "mov.b64 b, {%4, %5};\n\t"
-        "@q st.relaxed.gpu.global.v2.b64 [%0], {a, b};\n\t}"
-        :: "l"(p), "r"(pred), "r"(v0), "r"(t0), "r"(v1), "r"(t1) : "memory");
+        "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\t"
+        "@q st.relaxed.gpu.global.v4.b32 [%0], {%2, %3, %4, %5};\n\t}"
+        :: "l"(p), "r"(pred), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]) : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\t"
+        "@q st.relaxed.gpu.global.v2.b32 [%0], {%2, %3};\n\t}"
+        :: "l"(p), "r"(pred), "r"(v[0]), "r"(v[1]) : "memory");
+#endif
 }
 
-// one anti-diagonal step of the compute warp: lane j computes the 2x4 block
-// rows r0 = 2(s-j), r0+1, columns 4j..4j+3 of the strip
+// one anti-diagonal step of the compute warp: lane j computes the RPS x 4
+// block rows r0 = RPS(s-j) .. r0+RPS-1, columns 4j..4j+3 of the strip
+__device__ __forceinline__ int ring_wrap(int r) { return r >= RING_ROWS ? r - RING_ROWS : r; }
+__device__ __forceinline__ int ring_mod(int r) {
+    int m = r % RING_ROWS;
+    return m < 0 ? m + RING_ROWS : m;
+}
+
+// rm = r0 mod RING_ROWS (RPS | RING_ROWS, so rows r0 .. r0+RPS-1 never straddle the wrap)
 template <bool GUARD>
-__device__ __forceinline__ void nw_step(Lane& c, int s, int lane, uint32_t ring_lane, uint32_t bnd, int p2,
-                                        int n, unsigned long long* my_bnd, unsigned tagp1, int4& a_nx, int4& b_nx) {
-    const int r0 = 2 * (s - lane);
-    const uint32_t addr = ring_lane + (uint32_t)((r0 & (RING_ROWS - 1)) * ROW_BYTES);
-    const int4 a = a_nx, b = b_nx;                      // sim rows r0, r0 + 1 (loaded one step ahead)
-    {
-        const uint32_t nx = ring_lane + (uint32_t)(((r0 + 2) & (RING_ROWS - 1)) * ROW_BYTES);
-        a_nx = lds128(nx);
-        b_nx = lds128(nx + ROW_BYTES);
+__device__ __forceinline__ void nw_step(Lane& c, int s, int lane, int4* ring_lane, uint32_t bnd, int p2, int n,
+                                        int* pub_row, int rm) {
+    const int r0 = RPS * (s - lane);
+    int4* cur_p = ring_lane + (rm << 5);
+    const int4* pf_p = ring_lane + (ring_wrap(rm + 2 * RPS) << 5);
+    int4 cur[RPS];
+    int lb[RPS];
+#pragma unroll
+    for (int q = 0; q < RPS; ++q) {
+        cur[q] = c.nx1[q];
+        c.nx1[q] = c.nx2[q];
+        c.nx2[q] = pf_p[q * (STRIP / 4)];
+        lb[q] = c.bv[q];
     }
-    // lane 0's left values: boundary rows 2s, 2s + 1 (readiness checked per 4 steps)
-    const int2 bv = lds64v(bnd + (uint32_t)(((2 * s) & (RING_ROWS - 1)) * 4));
-    // lane j-1 finished rows r0, r0 + 1 in the previous step
-    const int sl0 = __shfl_up_sync(0xffffffffu, c.vs3, 1);
-    const int sl1 = __shfl_up_sync(0xffffffffu, c.ws3, 1);
-    const int left0 = lane == 0 ? bv.x : sl0;
-    const int left1 = lane == 0 ? bv.y : sl1;
-    // row r0 (up = h, diagonal = dprev / h), then row r0 + 1 (up = v)
-    const int v0 = max(max(a.x + c.dprev + p2, c.h0), left0);
-    const int v1 = max(max(a.y + c.h0 + p2, c.h1), v0);
-    const int v2 = max(max(a.z + c.h1 + p2, c.h2), v1);
-    const int v3 = max(max(a.w + c.h2 + p2, c.h3), v2);
-    const int w0 = max(max(b.x + left0 + p2, v0), left1);
-    const int w1 = max(max(b.y + v0 + p2, v1), w0);
-    const int w2 = max(max(b.z + v1 + p2, v2), w1);
-    const int w3 = max(max(b.w + v2 + p2, v3), w2);
+    ldsv<RPS>(bnd + (uint32_t)(((RPS * (s + 1)) & (BND_ROWS - 1)) * 4), c.bv);   // next step's boundary
+    int left[RPS];
+#pragma unroll
+    for (int q = 0; q < RPS; ++q) {
+        const int sl = __shfl_up_sync(0xffffffffu, c.send[q], 1);
+        left[q] = lane == 0 ? lb[q] : sl;
+    }
     const bool live = !GUARD || r0 >= 0;                // lanes start one step apart
-    if (live) {
-        sts128(addr, v0, v1, v2, v3);                   // S' replaces sim in place
-        sts128(addr + ROW_BYTES, w0, w1, w2, w3);
+    int up0 = c.h[0], up1 = c.h[1], up2 = c.h[2], up3 = c.h[3];
+    int d = c.dprev;
+#pragma unroll
+    for (int q = 0; q < RPS; ++q) {
+        const int x0 = max(max(cur[q].x + d + p2, up0), left[q]);
+        const int x1 = max(max(cur[q].y + up0 + p2, up1), x0);
+        const int x2 = max(max(cur[q].z + up1 + p2, up2), x1);
+        const int x3 = max(max(cur[q].w + up2 + p2, up3), x2);
+        if (live) cur_p[q * (STRIP / 4)] = make_int4(x0, x1, x2, x3);   // S' replaces sim in place
+        up0 = x0; up1 = x1; up2 = x2; up3 = x3;
+        d = left[q];
+        c.send[q] = live ? x3 : c.send[q];
     }
-    c.h0 = live ? w0 : c.h0;
-    c.h1 = live ? w1 : c.h1;
-    c.h2 = live ? w2 : c.h2;
-    c.h3 = live ? w3 : c.h3;
-    c.dprev = live ? left1 : c.dprev;
-    c.vs3 = live ? v3 : c.vs3;
-    c.ws3 = live ? w3 : c.ws3;
+    c.h[0] = live ? up0 : c.h[0];
+    c.h[1] = live ? up1 : c.h[1];
+    c.h[2] = live ? up2 : c.h[2];
+    c.h[3] = live ? up3 : c.h[3];
+    c.dprev = live ? d : c.dprev;
     // the strip's last column goes to the right neighbour (lane 31, rows < n)
-    publish2(my_bnd + r0, (lane == 31) & (r0 < n) & live, v3, tagp1 + (unsigned)r0, w3, tagp1 + 1u + (unsigned)r0);
+    const int pub = (lane == 31) & (r0 < n) & live;
+    publish(pub_row, pub, c.send);
 }
 
-// 16 steps (32 rows of lane 0); boundary readiness is checked every 4 steps
-// with a value prefetched 4 steps earlier
+// one block of STEPS steps (32 rows of lane 0); boundary readiness is checked
+// every GRP steps against a counter value prefetched GRP steps earlier
 template <bool GUARD>
-__device__ __forceinline__ void nw_block(Lane& c, int k, int lane, uint32_t ring_lane, uint32_t bnd, int p2, int n,
-                                         unsigned long long* my_bnd, unsigned tagp1, int& rd, const int* ready,
-                                         int4& a_nx, int4& b_nx) {
+__device__ __forceinline__ void nw_block(Lane& c, int k, int lane, int4* ring_lane, uint32_t bnd, int p2, int n,
+                                         int* my_bnd, int& rd, const int* ready, int rows_total) {
+    int* pub_blk = my_bnd + RPS * (k * STEPS - lane);  // lane 31's rows of step u: + RPS*u
+    int rm = ring_mod(k * BLK - RPS * lane);
 #pragma unroll
     for (int u = 0; u < STEPS; ++u) {
-        if ((u & 3) == 0) {
-            const int need = 2 * (k * STEPS + u) + 8;
+        const int s = k * STEPS + u;
+        if (u % GRP == 0) {                             // rows used (and prefetched) through step s + GRP
+            const int need = min(RPS * (s + GRP + 1), rows_total);   // the helper stops at rows_total
             while (rd < need) rd = ldv(ready);
             rd = ldv(ready);
         }
-        nw_step<GUARD>(c, k * STEPS + u, lane, ring_lane, bnd, p2, n, my_bnd, tagp1, a_nx, b_nx);
+        nw_step<GUARD>(c, s, lane, ring_lane, bnd, p2, n, pub_blk + RPS * u, rm);
+        rm = ring_wrap(rm + RPS);
     }
 }
 
 __global__ void __launch_bounds__(128, 1)
 nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, int p, int strips_per_matrix,
-          int total_strips, int* __restrict__ ticket, unsigned long long* __restrict__ bnd_g, unsigned epoch) {
+          int total_strips, int* __restrict__ ticket, int* __restrict__ bnd_g) {
     extern __shared__ __align__(16) unsigned char smem[];
     int32_t* ring_gen = reinterpret_cast<int32_t*>(smem);
-    Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem + RING_BYTES + BND_BYTES);
+    Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem + RING_BYTES + BND_BYTES + MBAR_BYTES);
     const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     const uint32_t bnd = ring + RING_BYTES;
+    const uint32_t mbar = bnd + BND_BYTES;
+    int gblk = 0;                                    // producer: blocks issued in earlier strips
+    if (threadIdx.x < NSLOT)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" :: "r"(mbar + 8u * threadIdx.x) : "memory");
     const int lane = threadIdx.x & 31;
     const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);   // warp-uniform role
     const int n_pad = (n + BLK - 1) / BLK * BLK;
     const int nblocks = n_pad / BLK;
-    const unsigned tag = (epoch & 0x7FFu) << 21;     // rows are < 2^20
 
     for (;;) {
         if (threadIdx.x == 0) {
@@ -251,106 +292,136 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
         __syncthreads();
         const int strip = ctrl->strip;
         NW_PROBE(6000000 + strip);
+        if (threadIdx.x == 0) NW_TRACE(1, 2047 - 0 * strip);
+        if (threadIdx.x == 0 && strip < total_strips) g_nw_trace_strip(strip);
         if (strip >= total_strips) return;
         const int bm = strip / strips_per_matrix;
         const int w = strip - bm * strips_per_matrix;
         const int col0 = w * STRIP;
-        unsigned long long* my_bnd = bnd_g + (long long)strip * n_pad;
+        int* my_bnd = bnd_g + (long long)strip * n_pad;
 
         if (warp == 0) {
             // ---------------- compute ----------------
-            Lane c = {0, 0, 0, 0, 0, 0, 0};
+            Lane c;
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) c.h[q] = 0;
+#pragma unroll
+            for (int q = 0; q < RPS; ++q) c.send[q] = 0;
+            c.dprev = 0;
             const int p2 = 2 * p;
-            const uint32_t ring_lane = ring + 16u * lane;
-            const unsigned tagp1 = tag + 1u;
+            int4* ring4 = reinterpret_cast<int4*>(smem);
             int pl = ldv(&ctrl->loaded);
             int rd = ldv(&ctrl->ready);
-            int4 a_nx = make_int4(0, 0, 0, 0), b_nx = make_int4(0, 0, 0, 0);
             for (int k = 0; k < nblocks + DRAIN; ++k) {
                 NW_PROBE(1000000 + k);
                 if (lane == 0) NW_TRACE(0, k);
-                if (k >= 3) {                           // lane 31 finished block k-3 at step 16k-2
+                if (k >= BLAG) {                        // lane 31 has finished block k - BLAG
                     __syncwarp();
-                    if (lane == 0) stv(&ctrl->computed, k - 3);
+                    if (lane == 0) stv(&ctrl->computed, k - BLAG);
                 }
-                // the last step of block k prefetches block k+1's first rows: need both
+                // the last steps of block k prefetch block k+1's first rows: need both
                 const int need_blk = min(k + 1, nblocks + DRAIN - 1);
                 while (pl < need_blk) pl = ldv(&ctrl->loaded);
-                if (k == 0) {                           // first step's operands
-                    const uint32_t a0 = ring_lane + (uint32_t)(((-2 * lane) & (RING_ROWS - 1)) * ROW_BYTES);
-                    a_nx = lds128(a0);
-                    b_nx = lds128(a0 + ROW_BYTES);
+                if (k == 0) {                           // operands of the first two steps
+                    while (rd < RPS) rd = ldv(&ctrl->ready);
+#pragma unroll
+                    for (int q = 0; q < RPS; ++q) {
+                        c.nx1[q] = ring4[ring_mod(-RPS * lane + q) * (STRIP / 4) + lane];
+                        c.nx2[q] = ring4[ring_mod(RPS - RPS * lane + q) * (STRIP / 4) + lane];
+                    }
+                    ldsv<RPS>(bnd, c.bv);
                 }
                 pl = ldv(&ctrl->loaded);                // prefetch for the next block
-                if (k < 2)
-                    nw_block<true>(c, k, lane, ring_lane, bnd, p2, n, my_bnd, tagp1, rd, &ctrl->ready, a_nx, b_nx);
+                if (k < (31 + STEPS - 1) / STEPS)
+                    nw_block<true>(c, k, lane, ring4 + lane, bnd, p2, n, my_bnd, rd, &ctrl->ready, (nblocks + DRAIN) * BLK);
                 else
-                    nw_block<false>(c, k, lane, ring_lane, bnd, p2, n, my_bnd, tagp1, rd, &ctrl->ready, a_nx, b_nx);
+                    nw_block<false>(c, k, lane, ring4 + lane, bnd, p2, n, my_bnd, rd, &ctrl->ready, (nblocks + DRAIN) * BLK);
             }
             __syncwarp();
             if (lane == 0) stv(&ctrl->computed, nblocks + DRAIN - 1);
         } else if (warp == 1) {
             // ---------------- producer: sim blocks -> ring ----------------
+            // Issues block k once its ring slot is flushed; each block's
+            // copies arrive on a per-slot mbarrier, polled without blocking so
+            // `loaded` is published as soon as a block lands.
             const int32_t* simb = sim + (long long)bm * n * n;
             const bool vec = (n & 3) == 0;
-            for (int k = 0; k < nblocks + DRAIN; ++k) {
-                NW_PROBE(2000000 + k);
-                if (k >= NSLOT) {
-                    while (ldv(&ctrl->flushed) < k - NSLOT) __nanosleep(128);
-                }
-                if (k < nblocks) {
-                    const int rows = min(BLK, n - k * BLK);
-                    uint32_t dst = ring + (uint32_t)((k & (NSLOT - 1)) * BLK * ROW_BYTES);
-                    if (vec) {
-                        const bool ok = col0 + CPL * lane < n;
-                        const int32_t* src = simb + (long long)k * BLK * n + col0 + CPL * lane;
-                        dst += 16u * lane;
+            const int total_blocks = nblocks + DRAIN;
+            int issued = 0, landed = 0;
+            while (landed < total_blocks) {
+                bool progress = false;
+                if (issued < total_blocks && (issued < NSLOT || ldv(&ctrl->flushed) >= issued - NSLOT)) {
+                    const int k = issued;
+                    const uint32_t mb = mbar + 8u * (uint32_t)((gblk + k) % NSLOT);
+                    if (k < nblocks) {
+                        const int rows = min(BLK, n - k * BLK);
+                        uint32_t dst = ring + (uint32_t)((k % NSLOT) * BLK * ROW_BYTES);
+                        if (vec) {
+                            const bool ok = col0 + CPL * lane < n;
+                            const int32_t* src = simb + (long long)k * BLK * n + col0 + CPL * lane;
+                            dst += 16u * lane;
 #pragma unroll 8
-                        for (int r = 0; r < rows; ++r) {
-                            if (ok) cp_async16(dst, src);
-                            dst += ROW_BYTES;
-                            src += n;
-                        }
-                    } else {
-                        const int32_t* src = simb + (long long)k * BLK * n + col0 + lane;
-                        dst += 4u * lane;
-                        for (int r = 0; r < rows; ++r) {
+                            for (int r = 0; r < rows; ++r) {
+                                if (ok) cp_async16(dst, src);
+                                dst += ROW_BYTES;
+                                src += n;
+                            }
+                        } else {
+                            const int32_t* src = simb + (long long)k * BLK * n + col0 + lane;
+                            dst += 4u * lane;
+                            for (int r = 0; r < rows; ++r) {
 #pragma unroll
-                            for (int q = 0; q < CPL; ++q)
-                                if (col0 + 32 * q + lane < n) cp_async4(dst + 128u * q, src + 32 * q);
-                            dst += ROW_BYTES;
-                            src += n;
+                                for (int q = 0; q < CPL; ++q)
+                                    if (col0 + 32 * q + lane < n) cp_async4(dst + 128u * q, src + 32 * q);
+                                dst += ROW_BYTES;
+                                src += n;
+                            }
                         }
+                        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(mb) : "memory");
+                    } else {
+                        asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}"
+                                     :: "r"(mb) : "memory");
+                    }
+                    ++issued;
+                    progress = true;
+                }
+                if (landed < issued) {
+                    const int g = gblk + landed;
+                    uint32_t ok;
+                    asm volatile("{\n\t.reg .pred p;\n\t"
+                                 "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                                 "selp.u32 %0, 1, 0, p;\n\t}"
+                                 : "=r"(ok) : "r"(mbar + 8u * (uint32_t)(g % NSLOT)), "r"((g / NSLOT) & 1)
+                                 : "memory");
+                    if (__all_sync(0xffffffffu, ok)) {
+                        if (lane == 0) {
+                            stv(&ctrl->loaded, landed);
+                            NW_TRACE(1, landed);
+                        }
+                        ++landed;
+                        progress = true;
                     }
                 }
-                cp_async_commit();
-                if (k >= 2) {
-                    cp_async_wait<2>();
-                    __syncwarp();
-                    if (lane == 0) { stv(&ctrl->loaded, k - 2); NW_TRACE(1, k - 2); }
-                }
+                if (!progress) __nanosleep(64);
             }
-            cp_async_wait<0>();
-            __syncwarp();
-            if (lane == 0) stv(&ctrl->loaded, nblocks + DRAIN - 1);
+            gblk += total_blocks;
         } else if (warp == 2) {
             // ---------------- boundary: left strip's last column -> shared ring ----------------
             // Lane l polls row 32m + l; rows are handed to the compute warp in
             // order through ctrl->ready as soon as a prefix of the group is in.
-            const unsigned long long* left = my_bnd - n_pad;
+            const int* left = my_bnd - n_pad;
             const int groups = nblocks + DRAIN;
             for (int m = 0; m < groups; ++m) {
                 const int r = m * BLK + lane;
                 NW_PROBE(3000000 + r);
-                if (m >= NSLOT) {
-                    while (ldv(&ctrl->computed) < m - NSLOT) __nanosleep(128);
+                if (m >= BND_GROUPS) {
+                    while (ldv(&ctrl->computed) < m - BND_GROUPS) __nanosleep(128);
                 }
                 int v = 0;                              // S'[r+1][0] = 0 on the matrix edge
                 bool ok = true;
                 if (w > 0 && r < n) {
-                    const unsigned long long x = ld_tagged(left + r);
-                    ok = (unsigned)(x >> 32) == (tag | (unsigned)(r + 1));
-                    v = (int)(unsigned)x;
+                    v = ld_bnd(left + r);
+                    ok = v != NW_EMPTY;
                 }
                 bool written = false;
                 int told = 0;
@@ -358,7 +429,7 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                     const unsigned ball = __ballot_sync(0xffffffffu, ok);
                     const int t = ball == 0xffffffffu ? 32 : __ffs(~ball) - 1;   // ready prefix
                     if (ok && !written && lane < t) {
-                        asm volatile("st.shared.b32 [%0], %1;" :: "r"(bnd + (uint32_t)((r & (RING_ROWS - 1)) * 4)),
+                        asm volatile("st.shared.b32 [%0], %1;" :: "r"(bnd + (uint32_t)((r & (BND_ROWS - 1)) * 4)),
                                      "r"(v) : "memory");
                         written = true;
                     }
@@ -370,9 +441,8 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                     if (t == 32) break;
                     __nanosleep(NW_POLL_NS);
                     if (!ok) {
-                        const unsigned long long x = ld_tagged(left + r);
-                        ok = (unsigned)(x >> 32) == (tag | (unsigned)(r + 1));
-                        v = (int)(unsigned)x;
+                        v = ld_bnd(left + r);
+                        ok = v != NW_EMPTY;
                     }
                 }
                 if (lane == 31) NW_TRACE(2, m);
@@ -388,9 +458,27 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                 NW_PROBE(5000000 + k);
                 while (ldv(&ctrl->computed) < k) __nanosleep(64);
                 const int rows = min(BLK, n - k * BLK);
-                const int32_t* src = ring_gen + (k & (NSLOT - 1)) * BLK * STRIP + lane;
+                const int32_t* src = ring_gen + (k % NSLOT) * BLK * STRIP + lane;
                 int32_t* dst = sc + (long long)(k * BLK + 1) * ld + col0 + 1 + lane;
                 int off = (k * BLK + col0 + lane + 2) * p;     // (i + j) * p of column lane, row k*BLK
+                if (rows == BLK && col0 + STRIP <= n) {
+                    // full block: 16 rows of loads in flight before their stores
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        int v[16][CPL];
+#pragma unroll
+                        for (int r = 0; r < 16; ++r)
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) v[r][q] = src[(16 * h + r) * STRIP + 32 * q];
+#pragma unroll
+                        for (int r = 0; r < 16; ++r) {
+                            int32_t* d = dst + (16 * h + r) * ld;
+                            const int o = off + (16 * h + r) * p;
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) d[32 * q] = v[r][q] - (o + 32 * q * p);
+                        }
+                    }
+                } else {
 #pragma unroll 4
                 for (int r = 0; r < rows; ++r) {
 #pragma unroll
@@ -399,6 +487,7 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                     dst += ld;
                     src += STRIP;
                     off += p;
+                }
                 }
                 __syncwarp();
                 if (lane == 0) { stv(&ctrl->flushed, k); NW_TRACE(3, k); }
@@ -429,28 +518,23 @@ extern "C" int lego_nw_debug_snapshot(int* out, int count) {
 }
 #endif
 
-// Boundary words + tickets, kept per (device, stream) across calls: words are
-// tagged with a launch epoch, so a launch never mistakes a previous launch's
-// word for its own; tickets are one counter per epoch.  The buffer is zeroed
-// when it is (re)allocated and whenever the 11-bit epoch wraps.  Launches on
-// one stream are ordered, so sharing the buffer between them is safe.
+// Boundary words + ticket, kept per (device, stream) across calls (launches
+// on one stream are ordered, so they can share it); every launch presets the
+// words it uses to NW_EMPTY and the ticket to 0.
 struct NwScratch {
     char* buf = nullptr;
     size_t bytes = 0;
-    unsigned epoch = 0;
 };
-constexpr size_t NW_TICKETS = 2048 * sizeof(int);
+constexpr size_t NW_TICKET_BYTES = 256;
 
-static lego_status nw_scratch(cudaStream_t st, size_t bnd_bytes, int** ticket, unsigned long long** bnd,
-                              unsigned* epoch) {
+static lego_status nw_scratch(cudaStream_t st, size_t bnd_bytes, int** ticket, int** bnd) {
     static std::mutex mu;
     static std::map<std::pair<int, cudaStream_t>, NwScratch> cache;
     int dev = 0;
     LEGO_TRY(lego_cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
     std::lock_guard<std::mutex> lk(mu);
     NwScratch& e = cache[std::make_pair(dev, st)];
-    const size_t need = NW_TICKETS + bnd_bytes;
-    bool zero = false;
+    const size_t need = NW_TICKET_BYTES + bnd_bytes;
     if (e.bytes < need) {
         if (e.buf) LEGO_TRY(lego_cuda_check(cudaFreeAsync(e.buf, st), "cudaFreeAsync"));
         e.buf = nullptr;
@@ -458,20 +542,11 @@ static lego_status nw_scratch(cudaStream_t st, size_t bnd_bytes, int** ticket, u
         const size_t grow = need + need / 4;
         LEGO_TRY(lego_cuda_check(cudaMallocAsync((void**)&e.buf, grow, st), "cudaMallocAsync"));
         e.bytes = grow;
-        zero = true;
     }
-    e.epoch = (e.epoch + 1) & 0x7FFu;
-    if (e.epoch == 0) {
-        e.epoch = 1;
-        zero = true;
-    }
-    if (zero) {
-        LEGO_TRY(lego_cuda_check(cudaMemsetAsync(e.buf, 0, e.bytes, st), "cudaMemsetAsync"));
-        e.epoch = 1;
-    }
-    *ticket = reinterpret_cast<int*>(e.buf) + e.epoch;
-    *bnd = reinterpret_cast<unsigned long long*>(e.buf + NW_TICKETS);
-    *epoch = e.epoch;
+    LEGO_TRY(lego_cuda_check(cudaMemsetAsync(e.buf, 0, NW_TICKET_BYTES, st), "cudaMemsetAsync"));
+    LEGO_TRY(lego_cuda_check(cudaMemsetAsync(e.buf + NW_TICKET_BYTES, 0x80, bnd_bytes, st), "cudaMemsetAsync"));
+    *ticket = reinterpret_cast<int*>(e.buf);
+    *bnd = reinterpret_cast<int*>(e.buf + NW_TICKET_BYTES);
     return LEGO_OK;
 }
 
@@ -493,11 +568,10 @@ extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n
     const long long total = (long long)strips * batch;
     if (total > INT32_MAX) return lego_fail(LEGO_E_SHAPE, "NW batch too large");
     const long long n_pad = (n + BLK - 1) / BLK * BLK;
-    const size_t bnd_bytes = sizeof(unsigned long long) * (size_t)total * (size_t)n_pad;
+    const size_t bnd_bytes = sizeof(int) * (size_t)total * (size_t)n_pad;
     int* ticket = nullptr;
-    unsigned long long* bnd_g = nullptr;
-    unsigned epoch = 0;
-    LEGO_TRY(nw_scratch(st, bnd_bytes, &ticket, &bnd_g, &epoch));
+    int* bnd_g = nullptr;
+    LEGO_TRY(nw_scratch(st, bnd_bytes, &ticket, &bnd_g));
     static cudaError_t attr = cudaFuncSetAttribute(nw_strips, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    SMEM_BYTES);
     LEGO_TRY(lego_cuda_check(attr, "cudaFuncSetAttribute(nw)"));
@@ -518,6 +592,6 @@ extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long long ctas = total < sms ? total : sms;      // one strip CTA per SM, persistent
     nw_strips<<<(unsigned)ctas, 128, SMEM_BYTES, st>>>(sim, score, (int)n, penalty, strips, (int)total, ticket,
-                                                       bnd_g, epoch);
+                                                       bnd_g);
     return lego_cuda_check(cudaGetLastError(), "nw launch");
 }
