@@ -70,7 +70,7 @@ constexpr int MBAR_BYTES = NSLOT * 8;
 constexpr int CTRL_BYTES = 64;
 constexpr int SMEM_BYTES = RING_BYTES + BND_BYTES + MBAR_BYTES + CTRL_BYTES;
 #ifndef NW_POLL_NS
-#define NW_POLL_NS 32                                // boundary poll back-off
+#define NW_POLL_NS 0                                 // boundary poll back-off
 #endif
 
 #ifdef LEGO_NW_DEBUG
@@ -439,7 +439,7 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                         told = t;
                     }
                     if (t == 32) break;
-                    __nanosleep(NW_POLL_NS);
+                    if (NW_POLL_NS) __nanosleep(NW_POLL_NS);
                     if (!ok) {
                         v = ld_bnd(left + r);
                         ok = v != NW_EMPTY;
