@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "lego_common.h"
@@ -299,6 +300,234 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     }
 }
 
+// ===========================================================================
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a
+// 256 x 256 output tile with tcgen05.mma.cta_group::2 (M = 256): each CTA
+// stages its own 128 rows of A and its own 128-row half of B (so every
+// operand byte crosses L2 -> SM once per pair instead of twice), the leader
+// CTA's single thread issues the MMAs for both, and each CTA's TMEM holds its
+// 128 accumulator rows.  Barrier protocol:
+//   full[s]     leader only; the leader arrives with expect_tx(both CTAs'
+//               bytes) and both CTAs' TMA loads complete_tx on it
+//   empty[s]    both CTAs; the leader's tcgen05.commit multicasts to both
+//   acc_full[a] both CTAs; multicast commit after a tile's last k-block
+//   acc_empty[a] leader only; the 4 epilogue warps of each CTA arrive (8)
+namespace pair {
+
+constexpr int BM = 128;                              // rows of A per CTA (pair M = 256)
+constexpr int BN = 256;                              // pair N (each CTA stages 128 rows of B)
+constexpr int BNH = BN / 2;
+constexpr int BK = 64;
+constexpr int STAGES = 6;
+constexpr int A_BYTES = BM * BK * 2;                 // 16 KiB
+constexpr int B_BYTES = BNH * BK * 2;                // 16 KiB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_THREADS = 192;
+constexpr int ACC_COLS = BN;
+constexpr int TMEM_COLS = 2 * ACC_COLS;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_to_cta(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(cluster_addr) : "memory");
+}
+// TMA into this CTA's smem, completion signalled on an mbarrier of either CTA of the pair
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];"
+        :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit2(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 :: "r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
+}
+
+__host__ __device__ constexpr uint32_t make_idesc2() {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t((2 * BM) >> 4) << 24);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                       __nv_bfloat16* __restrict__ C, int M, int N, int K, int batch, int raster_mode) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    unsigned char* sA = smem;
+    unsigned char* sB = smem + STAGES * A_BYTES;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty_bar = full_bar + STAGES;
+    uint64_t* acc_full = empty_bar + STAGES;       // [2]
+    uint64_t* acc_empty = acc_full + 2;            // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int kblocks = K / BK;
+    // tiles are 256 x 256 output blocks: "m-blocks" of 256 rows
+    Raster ras{M / (2 * BM), N / BN, (M / (2 * BM)) * (N / BN), raster_mode > 0 ? raster_mode : 1};
+    const int total_tiles = ras.per_batch * batch;
+    const int pair_id = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmap_a);
+        prefetch_tmap(&tmap_b);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&acc_full[a], 1);
+            mbar_init(&acc_empty[a], 8);            // 4 epilogue warps x 2 CTAs
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(tmem_slot)), "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    // the leader's barriers, as shared::cluster addresses
+    const uint32_t full_leader = map_to_cta(smem_u32(full_bar), 0);
+    const uint32_t acc_empty_leader = map_to_cta(smem_u32(acc_empty), 0);
+
+    auto coords = [&](int t, int& b, int& m, int& n) {
+        if (raster_mode) ras.coords(t, b, m, n);
+        else { b = t / ras.per_batch; int r = t - b * ras.per_batch; m = r / ras.nb; n = r - m * ras.nb; }
+    };
+
+    if (warp == 0) {
+        // ===================== TMA producer (both CTAs) =====================
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = pair_id; t < total_tiles; t += num_pairs) {
+                int b, mb, nb;
+                coords(t, b, mb, nb);
+                const int arow = mb * 2 * BM + (int)rank * BM;
+                const int brow = nb * BN + (int)rank * BNH;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                    if (leader) mbar_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
+                    const uint32_t fb = full_leader + 8u * stage;
+                    tma_load_3d_pair(sA + stage * A_BYTES, &tmap_a, fb, kb * BK, arow, b);
+                    tma_load_3d_pair(sB + stage * B_BYTES, &tmap_b, fb, kb * BK, brow, b);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (leader CTA only) =====================
+        if (leader) {
+            constexpr uint32_t idesc = make_idesc2();
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int t = pair_id; t < total_tiles; t += num_pairs, ++it) {
+                const int acc = it & 1;
+                const uint32_t acc_phase = (it >> 1) & 1;
+                mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * ACC_COLS;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full_bar[stage], phase);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+                        const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+                        for (int k = 0; k < BK / UMMA_K; ++k)
+                            tc_mma2(d_tmem, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc,
+                                    (kb | k) != 0);
+                        tc_commit2(&empty_bar[stage]);
+                        if (kb == kblocks - 1) tc_commit2(&acc_full[acc]);
+                    }
+                    __syncwarp();
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else {
+        // ===================== epilogue (warps 2..5, both CTAs) =====================
+        const int quarter = warp & 3;
+        int it = 0;
+        for (int t = pair_id; t < total_tiles; t += num_pairs, ++it) {
+            int b, mb, nb;
+            coords(t, b, mb, nb);
+            const int acc = it & 1;
+            mbar_wait(&acc_full[acc], (it >> 1) & 1);
+            tc_fence_after();
+            const int row = mb * 2 * BM + (int)rank * BM + quarter * 32 + lane;
+            __nv_bfloat16* crow = C + (static_cast<size_t>(b) * M + row) * static_cast<size_t>(N) + nb * BN;
+            const uint32_t taddr = tmem_base + acc * ACC_COLS + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t v[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+                      "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+                      "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr + c));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                uint4* dst = reinterpret_cast<uint4*>(crow + c);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 o;
+                    o.x = pack_bf16(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
+                    o.y = pack_bf16(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
+                    o.z = pack_bf16(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
+                    o.w = pack_bf16(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
+                    dst[q] = o;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8u * acc);
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "r"(TMEM_COLS));
+    }
+}
+
+}  // namespace pair
+
 // ---- host side ------------------------------------------------------------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -344,6 +573,33 @@ extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int
         return lego_fail(LEGO_E_SHAPE, "gemm dimensions too large");
     if (((uintptr_t)A | (uintptr_t)B | (uintptr_t)C) & 15)
         return lego_fail(LEGO_E_ARG, "gemm buffers must be 16-byte aligned");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static const bool pair_ok = [] {
+        const char* e = getenv("LEGO_GEMM_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    if (pair_ok && M % (2 * pair::BM) == 0 && N % pair::BN == 0) {
+        // CTA-pair kernel: 256 x 256 tiles on cta_group::2
+        CUtensorMap ma, mb;
+        LEGO_TRY(make_map(&ma, A, M, K, batch, pair::BM));
+        LEGO_TRY(make_map(&mb, B, N, K, batch, pair::BNH));
+        static std::once_flag pair_once;
+        static cudaError_t pair_err = cudaSuccess;
+        std::call_once(pair_once, [] {
+            pair_err = cudaFuncSetAttribute(pair::gemm_bf16_tcgen05_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            pair::SMEM_BYTES);
+        });
+        LEGO_TRY(lego_cuda_check(pair_err, "cudaFuncSetAttribute(gemm pair smem)"));
+        const int64_t tiles = (M / (2 * pair::BM)) * (N / pair::BN) * batch;
+        const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
+        pair::gemm_bf16_tcgen05_pair<<<(unsigned)(2 * pairs), pair::NUM_THREADS, pair::SMEM_BYTES,
+                                       static_cast<cudaStream_t>(stream)>>>(
+            ma, mb, static_cast<__nv_bfloat16*>(C), (int)M, (int)N, (int)K, (int)batch,
+            raster > 1 ? raster / 2 : raster);   // G counts 128-row m-blocks; pair tiles are 256 rows
+        return lego_cuda_check(cudaGetLastError(), "gemm pair launch");
+    }
     CUtensorMap ma, mb;
     LEGO_TRY(make_map(&ma, A, M, K, batch, BM));
     LEGO_TRY(make_map(&mb, B, N, K, batch, BN));
@@ -353,9 +609,6 @@ extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int
         attr_err = cudaFuncSetAttribute(gemm_bf16_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     });
     LEGO_TRY(lego_cuda_check(attr_err, "cudaFuncSetAttribute(gemm smem)"));
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t tiles = (M / BM) * (N / BN) * batch;
     const int grid = (int)(tiles < sms ? tiles : sms);
     gemm_bf16_tcgen05<<<grid, NUM_THREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(

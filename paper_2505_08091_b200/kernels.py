@@ -53,6 +53,8 @@ def _text(name: str) -> str:
 
 def _assemble(gen_body: str, defines: Dict[str, int]) -> str:
     """Program source: helpers + generated namespace + kernel templates."""
+    defines = {**defines, **({"LEGO_LDV": LOAD_HINT} if LOAD_HINT else {}),
+               **({"LEGO_STV": STORE_HINT} if STORE_HINT else {})}
     head = "".join(f"#define {k} {v}\n" for k, v in defines.items())
     return (head + _text("lego_index.cuh").replace("#pragma once", "") + "\nnamespace gen {\n"
             + gen_body + "}\n" + _text("remap_kernels.cuh").replace("#pragma once", ""))
@@ -178,6 +180,11 @@ BAND_ROWS, BAND_DIAGS = 64, 64
 # (scripts/quick_transpose.py, profiles/r01_transpose_variants.md): regT,
 # with smem for 1-byte elements
 TRANSPOSE_VARIANT = os.environ.get("LEGO_TRANSPOSE", "")
+# load / store cache-hint variants of the remap kernels (remap_kernels.cuh LEGO_LDV / LEGO_STV)
+# (measured: L2::256B sector promotion on loads, LEGO_LDV=1, +2.7% on the
+# headline transpose and +1.4% on the tiled gather; scripts/quick_hints.py)
+LOAD_HINT = int(os.environ.get("LEGO_LDV", "1"))
+STORE_HINT = int(os.environ.get("LEGO_STV", "0"))
 # warp-tile walk order of the transpose ("x", "y" or "block", see lower.transpose_plan)
 TILE_ORDER = os.environ.get("LEGO_TILE_ORDER", "block")
 # CTAs of the persistent transpose variant (2 resident CTAs x 148 SMs by default)
@@ -244,7 +251,7 @@ def _scatter_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
 
 def _remap_program(src_layout, dst_layout, elem_bytes):
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, TRANSPOSE_VARIANT,
-           BAND_ORDER, PERSIST_CTAS, TILE_ORDER)
+           BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT)
     plans = []
 
     def build():
