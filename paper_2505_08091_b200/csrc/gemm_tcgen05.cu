@@ -314,18 +314,28 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
 //   acc_empty[a] leader only; the 4 epilogue warps of each CTA arrive (8)
 namespace pair {
 
-constexpr int BM = 128;                              // rows of A per CTA (pair M = 256)
-constexpr int BN = 256;                              // pair N (each CTA stages 128 rows of B)
-constexpr int BNH = BN / 2;
-constexpr int BK = 64;
-constexpr int STAGES = 6;
-constexpr int A_BYTES = BM * BK * 2;                 // 16 KiB
-constexpr int B_BYTES = BNH * BK * 2;                // 16 KiB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int NUM_THREADS = 192;
-constexpr int ACC_COLS = BN;
-constexpr int TMEM_COLS = 2 * ACC_COLS;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+// NH = number of N=256 halves per pair tile: 1 -> 256 x 256 tiles with a
+// double-buffered accumulator (epilogue overlaps the next tile), 2 -> 256 x 512
+// tiles (each operand byte feeds 4/3 more FLOPs; the 512-column accumulator
+// fills TMEM, so the epilogue of a tile precedes the next tile's MMAs)
+template <int NH>
+struct Cfg {
+    static constexpr int BM = 128;                   // rows of A per CTA (pair M = 256)
+    static constexpr int BN = 256 * NH;              // pair N
+    static constexpr int BNH = 128 * NH;             // rows of B staged per CTA
+    static constexpr int BK = 64;
+    static constexpr int STAGES = NH == 1 ? 6 : 4;
+    static constexpr int A_BYTES = BM * BK * 2;      // 16 KiB
+    static constexpr int B_BYTES = BNH * BK * 2;     // 16 KiB per half
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    // warps: 0 TMA, 1 MMA, then 4 epilogue warps per 256 accumulator columns
+    static constexpr int NUM_THREADS = 64 + 128 * NH;
+    static constexpr int ACC_COLS = BN;
+    static constexpr int NBUF = NH == 1 ? 2 : 1;     // accumulator buffers in TMEM
+    static constexpr int TMEM_COLS = 512;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+};
+constexpr int BM = 128, BN = 256, BNH = 128, NUM_THREADS = 192;   // host-side geometry checks
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -365,13 +375,19 @@ __device__ __forceinline__ void tc_commit2(uint64_t* bar) {
                  :: "r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
 }
 
+// M = 256 (cta_group::2), N = 256 per instruction
 __host__ __device__ constexpr uint32_t make_idesc2() {
-    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t((2 * BM) >> 4) << 24);
+    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(256 >> 3) << 17) | (uint32_t(256 >> 4) << 24);
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+template <int NH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NH>::NUM_THREADS, 1)
 gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                        __nv_bfloat16* __restrict__ C, int M, int N, int K, int batch, int raster_mode) {
+    using C_ = Cfg<NH>;
+    constexpr int BM = C_::BM, BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES;
+    constexpr int A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+    constexpr int ACC_COLS = C_::ACC_COLS, NBUF = C_::NBUF, TMEM_COLS = C_::TMEM_COLS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -379,8 +395,8 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     unsigned char* sB = smem + STAGES * A_BYTES;
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty_bar = full_bar + STAGES;
-    uint64_t* acc_full = empty_bar + STAGES;       // [2]
-    uint64_t* acc_empty = acc_full + 2;            // [2]
+    uint64_t* acc_full = empty_bar + STAGES;       // [NBUF]
+    uint64_t* acc_empty = acc_full + 2;            // [NBUF]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int warp = threadIdx.x >> 5;
@@ -433,13 +449,16 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
                 int b, mb, nb;
                 coords(t, b, mb, nb);
                 const int arow = mb * 2 * BM + (int)rank * BM;
-                const int brow = nb * BN + (int)rank * BNH;
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     if (leader) mbar_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
                     const uint32_t fb = full_leader + 8u * stage;
                     tma_load_3d_pair(sA + stage * A_BYTES, &tmap_a, fb, kb * BK, arow, b);
-                    tma_load_3d_pair(sB + stage * B_BYTES, &tmap_b, fb, kb * BK, brow, b);
+                    // B half h: this CTA's 128 rows of the output columns [256h, 256h + 256)
+#pragma unroll
+                    for (int h = 0; h < NH; ++h)
+                        tma_load_3d_pair(sB + stage * B_BYTES + h * (128 * BK * 2), &tmap_b, fb, kb * BK,
+                                         nb * BN + h * 256 + (int)rank * 128, b);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -452,21 +471,49 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
             uint32_t phase = 0;
             int it = 0;
             for (int t = pair_id; t < total_tiles; t += num_pairs, ++it) {
-                const int acc = it & 1;
-                const uint32_t acc_phase = (it >> 1) & 1;
+                const int acc = NBUF == 2 ? (it & 1) : 0;
+                const uint32_t acc_phase = NBUF == 2 ? ((it >> 1) & 1) : (it & 1);
+                // NH == 2: acc_empty[h] = accumulator columns [256h, 256h+256) drained
                 mbar_wait(&acc_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * ACC_COLS;
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
+                    if (NH == 2 && kb == 0) {
+                        // first k-block: half 0 while the epilogue still drains half 1
+                        const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+                        const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+                        if (elect_one()) {
+#pragma unroll
+                            for (int k = 0; k < BK / UMMA_K; ++k)
+                                tc_mma2(d_tmem, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc,
+                                        k != 0);
+                        }
+                        __syncwarp();
+                        mbar_wait(&acc_empty[1], acc_phase ^ 1);
+                        tc_fence_after();
+                        if (elect_one()) {
+#pragma unroll
+                            for (int k = 0; k < BK / UMMA_K; ++k)
+                                tc_mma2(d_tmem + 256, smem_desc(a0 + k * UMMA_K * 2),
+                                        smem_desc(b0 + 128 * BK * 2 + k * UMMA_K * 2), idesc, k != 0);
+                            tc_commit2(&empty_bar[stage]);
+                            if (kb == kblocks - 1) tc_commit2(&acc_full[acc]);
+                        }
+                        __syncwarp();
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     if (elect_one()) {
                         const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
                         for (int k = 0; k < BK / UMMA_K; ++k)
-                            tc_mma2(d_tmem, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc,
-                                    (kb | k) != 0);
+#pragma unroll
+                            for (int h = 0; h < NH; ++h)
+                                tc_mma2(d_tmem + h * 256, smem_desc(a0 + k * UMMA_K * 2),
+                                        smem_desc(b0 + h * (128 * BK * 2) + k * UMMA_K * 2), idesc, (kb | k) != 0);
                         tc_commit2(&empty_bar[stage]);
                         if (kb == kblocks - 1) tc_commit2(&acc_full[acc]);
                     }
@@ -476,20 +523,25 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
             }
         }
     } else {
-        // ===================== epilogue (warps 2..5, both CTAs) =====================
+        // ===================== epilogue (warps 2.., both CTAs) =====================
+        // warp -> TMEM lane quarter (warp % 4) and accumulator half (NH == 2)
         const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;
+        constexpr int EPI_COLS = 256;                         // columns per epilogue warp
         int it = 0;
         for (int t = pair_id; t < total_tiles; t += num_pairs, ++it) {
             int b, mb, nb;
             coords(t, b, mb, nb);
-            const int acc = it & 1;
-            mbar_wait(&acc_full[acc], (it >> 1) & 1);
+            const int acc = NBUF == 2 ? (it & 1) : 0;
+            mbar_wait(&acc_full[acc], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
             tc_fence_after();
             const int row = mb * 2 * BM + (int)rank * BM + quarter * 32 + lane;
-            __nv_bfloat16* crow = C + (static_cast<size_t>(b) * M + row) * static_cast<size_t>(N) + nb * BN;
-            const uint32_t taddr = tmem_base + acc * ACC_COLS + (static_cast<uint32_t>(quarter * 32) << 16);
+            __nv_bfloat16* crow = C + (static_cast<size_t>(b) * M + row) * static_cast<size_t>(N) + nb * BN +
+                                  half * EPI_COLS;
+            const uint32_t taddr = tmem_base + acc * ACC_COLS + half * EPI_COLS +
+                                   (static_cast<uint32_t>(quarter * 32) << 16);
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
+            for (int c = 0; c < EPI_COLS; c += 32) {
                 uint32_t v[32];
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -515,7 +567,7 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8u * acc);
+            if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8u * (NH == 2 ? half : acc));
         }
     }
     tc_fence_before();
@@ -560,6 +612,31 @@ lego_status make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K
     return LEGO_OK;
 }
 
+template <int NH>
+lego_status launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t M, int64_t N, int64_t K,
+                        int64_t batch, int raster, int64_t pairs, void* stream) {
+    using C_ = pair::Cfg<NH>;
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    std::call_once(once, [] {
+        err = cudaFuncSetAttribute(pair::gemm_bf16_tcgen05_pair<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   C_::SMEM_BYTES);
+    });
+    LEGO_TRY(lego_cuda_check(err, "cudaFuncSetAttribute(gemm pair smem)"));
+    pair::gemm_bf16_tcgen05_pair<NH><<<(unsigned)(2 * pairs), C_::NUM_THREADS, C_::SMEM_BYTES,
+                                       static_cast<cudaStream_t>(stream)>>>(
+        ma, mb, static_cast<__nv_bfloat16*>(C), (int)M, (int)N, (int)K, (int)batch, raster);
+    return lego_cuda_check(cudaGetLastError(), "gemm pair launch");
+}
+
+bool pair_wide() {
+    static const bool w = [] {
+        const char* e = getenv("LEGO_GEMM_WIDE");
+        return !(e && e[0] == '0');
+    }();
+    return w;
+}
+
 }  // namespace
 
 extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
@@ -581,24 +658,16 @@ extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int
         return !(e && e[0] == '0');
     }();
     if (pair_ok && M % (2 * pair::BM) == 0 && N % pair::BN == 0) {
-        // CTA-pair kernel: 256 x 256 tiles on cta_group::2
+        // CTA-pair kernel on cta_group::2: 256 x 512 tiles when N allows, else 256 x 256
+        const bool wide = N % 512 == 0 && pair_wide();
         CUtensorMap ma, mb;
         LEGO_TRY(make_map(&ma, A, M, K, batch, pair::BM));
-        LEGO_TRY(make_map(&mb, B, N, K, batch, pair::BNH));
-        static std::once_flag pair_once;
-        static cudaError_t pair_err = cudaSuccess;
-        std::call_once(pair_once, [] {
-            pair_err = cudaFuncSetAttribute(pair::gemm_bf16_tcgen05_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            pair::SMEM_BYTES);
-        });
-        LEGO_TRY(lego_cuda_check(pair_err, "cudaFuncSetAttribute(gemm pair smem)"));
-        const int64_t tiles = (M / (2 * pair::BM)) * (N / pair::BN) * batch;
+        LEGO_TRY(make_map(&mb, B, N, K, batch, 128));
+        const int64_t tiles = (M / (2 * pair::BM)) * (N / (wide ? 512 : 256)) * batch;
         const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
-        pair::gemm_bf16_tcgen05_pair<<<(unsigned)(2 * pairs), pair::NUM_THREADS, pair::SMEM_BYTES,
-                                       static_cast<cudaStream_t>(stream)>>>(
-            ma, mb, static_cast<__nv_bfloat16*>(C), (int)M, (int)N, (int)K, (int)batch,
-            raster > 1 ? raster / 2 : raster);   // G counts 128-row m-blocks; pair tiles are 256 rows
-        return lego_cuda_check(cudaGetLastError(), "gemm pair launch");
+        const int g = raster > 1 ? raster / 2 : raster;   // G counts 128-row m-blocks; pair tiles are 256 rows
+        if (wide) return launch_pair<2>(ma, mb, C, M, N, K, batch, g, pairs, stream);
+        return launch_pair<1>(ma, mb, C, M, N, K, batch, g, pairs, stream);
     }
     CUtensorMap ma, mb;
     LEGO_TRY(make_map(&ma, A, M, K, batch, BM));

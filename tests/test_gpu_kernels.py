@@ -26,10 +26,14 @@ def _gemm_check(M, N, Kd, batch=1, raster=1, seed=5):
 
 
 def test_gemm_small_shapes():
-    _gemm_check(128, 256, 64)
-    _gemm_check(256, 512, 128, batch=2)
-    _gemm_check(384, 256, 1024, raster=0)
-    _gemm_check(2048, 1024, 512, batch=3)
+    # kernel selection by shape (csrc/gemm_tcgen05.cu): M % 256 and N % 512 -> CTA-pair 256x512
+    # tiles; M % 256 and N % 256 -> CTA-pair 256x256; otherwise single-CTA 128x256
+    _gemm_check(128, 256, 64)                   # single CTA
+    _gemm_check(256, 512, 128, batch=2)         # pair, 256x512
+    _gemm_check(384, 256, 1024, raster=0)       # single CTA
+    _gemm_check(2048, 1024, 512, batch=3)       # pair, 256x512
+    _gemm_check(512, 768, 256, raster=4)        # pair, 256x256
+    _gemm_check(1024, 1280, 192, batch=2)       # pair, 256x256 (N % 512 = 256)
 
 
 def test_gemm_8192_cubed():
