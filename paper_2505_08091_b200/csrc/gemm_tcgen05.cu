@@ -130,6 +130,20 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return r;
 }
 
+// 32 lanes x 32 consecutive fp32 accumulator columns (no wait)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+
 // LEGO raster: tile t -> (batch, m-block, n-block).  The layout
 //   GroupBy([MB/G, NB, G]).OrderBy(Row(MB/G, NB, G)),  inv(t) = (g, n, m_in)
 // lists tiles group by group (G m-blocks), n-blocks inside a group,
@@ -333,7 +347,8 @@ struct Cfg {
     static constexpr int ACC_COLS = BN;
     static constexpr int NBUF = NH == 1 ? 2 : 1;     // accumulator buffers in TMEM
     static constexpr int TMEM_COLS = 512;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int EPI_BYTES = 2048;           // per epilogue warp: 32 rows x 64 B staging
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + (NUM_THREADS / 32 - 2) * EPI_BYTES;
 };
 constexpr int BM = 128, BN = 256, BNH = 128, NUM_THREADS = 192;   // host-side geometry checks
 
@@ -398,6 +413,7 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     uint64_t* acc_full = empty_bar + STAGES;       // [NBUF]
     uint64_t* acc_empty = acc_full + 2;            // [NBUF]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    unsigned char* epi_stage = smem + STAGES * STAGE_BYTES + 256;      // [epilogue warp][32 rows][64 B]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -535,34 +551,40 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
             const int acc = NBUF == 2 ? (it & 1) : 0;
             mbar_wait(&acc_full[acc], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
             tc_fence_after();
-            const int row = mb * 2 * BM + (int)rank * BM + quarter * 32 + lane;
-            __nv_bfloat16* crow = C + (static_cast<size_t>(b) * M + row) * static_cast<size_t>(N) + nb * BN +
-                                  half * EPI_COLS;
+            const int row0 = mb * 2 * BM + (int)rank * BM + quarter * 32;      // this warp's 32 rows
+            __nv_bfloat16* cbase = C + (static_cast<size_t>(b) * M + row0) * static_cast<size_t>(N) + nb * BN +
+                                   half * EPI_COLS;
+            // staging: row r's 16-byte chunk q at r*64 + 16*(q ^ ((r >> 1) & 3)) -- conflict-free for
+            // both the row-per-lane writes and the 4-lanes-per-row reads
+            unsigned char* stg = epi_stage + (warp - 2) * C_::EPI_BYTES;
             const uint32_t taddr = tmem_base + acc * ACC_COLS + half * EPI_COLS +
                                    (static_cast<uint32_t>(quarter * 32) << 16);
 #pragma unroll 1
-            for (int c = 0; c < EPI_COLS; c += 32) {
-                uint32_t v[32];
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-                      "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-                      "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr + c));
+            for (int c = 0; c < EPI_COLS; c += 64) {
+                uint32_t v[2][32];                              // two chunks per TMEM round trip
+                tmem_ld32(taddr + c, v[0]);
+                tmem_ld32(taddr + c + 32, v[1]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                uint4* dst = reinterpret_cast<uint4*>(crow + c);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint4 o;
-                    o.x = pack_bf16(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
-                    o.y = pack_bf16(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
-                    o.z = pack_bf16(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
-                    o.w = pack_bf16(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
-                    dst[q] = o;
+                for (int h2 = 0; h2 < 2; ++h2) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 o;
+                        o.x = pack_bf16(__uint_as_float(v[h2][8 * q + 0]), __uint_as_float(v[h2][8 * q + 1]));
+                        o.y = pack_bf16(__uint_as_float(v[h2][8 * q + 2]), __uint_as_float(v[h2][8 * q + 3]));
+                        o.z = pack_bf16(__uint_as_float(v[h2][8 * q + 4]), __uint_as_float(v[h2][8 * q + 5]));
+                        o.w = pack_bf16(__uint_as_float(v[h2][8 * q + 6]), __uint_as_float(v[h2][8 * q + 7]));
+                        *reinterpret_cast<uint4*>(stg + lane * 64 + 16 * (q ^ ((lane >> 1) & 3))) = o;
+                    }
+                    __syncwarp();
+                    // 4 lanes per row: each store instruction writes 8 full 64-byte row segments
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int r = 8 * q + (lane >> 2), cq = lane & 3;
+                        const uint4 o = *reinterpret_cast<const uint4*>(stg + r * 64 + 16 * (cq ^ ((r >> 1) & 3)));
+                        *reinterpret_cast<uint4*>(cbase + static_cast<size_t>(r) * N + c + 32 * h2 + 8 * cq) = o;
+                    }
+                    __syncwarp();
                 }
             }
             tc_fence_before();
