@@ -123,7 +123,11 @@ lego_status lego_softmax_f32(const float *x, float *y, int64_t rows, int64_t col
  * sim is n x n; batch independent alignments back to back.
  * S[0][j] = -j*p, S[i][0] = -i*p,
  * S[i][j] = max(S[i-1][j-1] + sim[i-1][j-1], S[i-1][j] - p, S[i][j-1] - p).
- * Tiles are swept in anti-diagonal order with the LEGO antidiag layout. */
+ * Tiles are swept in anti-diagonal order with the LEGO antidiag layout.
+ * The kernel works on offset scores S + (i+j)p in int32: requires
+ * |p| * (2n + 2) < 2^30 (else LEGO_E_ARG) and scores within +-2^30.
+ * sim must be 16-byte aligned.  Stream-ordered; keeps a per-(device, stream)
+ * scratch buffer of strips x n int32 between calls. */
 lego_status lego_nw_i32(const int32_t *sim, int32_t *score, int64_t n, int32_t penalty,
                         int64_t batch, void *stream);
 

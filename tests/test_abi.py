@@ -45,6 +45,14 @@ def test_null_arguments_fail_cleanly():
     assert st == 3 and b"cols % 4" in lib.lego_last_error()
     with pytest.raises(L.ShapeMismatch):
         R.check(lib.lego_gemm_bf16(None, None, None, 100, 256, 64, 1, 1, None))
+    # NW: argument checks run before any CUDA call (offset-score range, alignment)
+    buf = ctypes.create_string_buffer(64 + 16)
+    aligned = (ctypes.addressof(buf) + 15) & ~15
+    st = lib.lego_nw_i32(aligned, aligned, 16384, 40000, 1, None)
+    assert st == 8 and b"penalty" in lib.lego_last_error()
+    st = lib.lego_nw_i32(aligned + 4, aligned, 16, 10, 1, None)
+    assert st == 8 and b"16-byte aligned" in lib.lego_last_error()
+    assert lib.lego_nw_i32(aligned, aligned, 16, 10, 0, None) == 0     # empty batch
 
 
 @pytest.mark.parametrize("dsl", [
