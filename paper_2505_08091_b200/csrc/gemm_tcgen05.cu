@@ -350,7 +350,7 @@ struct Cfg {
     static constexpr int EPI_BYTES = 2048;           // per epilogue warp: 32 rows x 64 B staging
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + (NUM_THREADS / 32 - 2) * EPI_BYTES;
 };
-constexpr int BM = 128, BN = 256, BNH = 128, NUM_THREADS = 192;   // host-side geometry checks
+constexpr int BM = 128, BN = 256;                    // host-side geometry checks (NH = 1 tile)
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;

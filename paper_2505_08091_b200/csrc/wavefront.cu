@@ -111,28 +111,9 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 
-__device__ __forceinline__ int4 lds128(uint32_t a) {
-    int4 v;
-    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-// volatile: re-read on every spin iteration (ptxas hoists weak loads out of loops)
-__device__ __forceinline__ int4 lds128v(uint32_t a) {
-    int4 v;
-    asm volatile("ld.volatile.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sts128(uint32_t a, int x, int y, int z, int w) {
-    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" :: "r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
-}
-__device__ __forceinline__ void sts64(uint32_t a, unsigned long long v) {
-    asm volatile("st.shared.b64 [%0], %1;" :: "r"(a), "l"(v) : "memory");
-}
 // boundary words start as NW_EMPTY (|S'| < 2^30 never equals it)
 constexpr int NW_EMPTY = (int)0x80808080;
 __device__ __forceinline__ int ld_bnd(const int* p) {
