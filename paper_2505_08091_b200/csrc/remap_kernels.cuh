@@ -183,6 +183,9 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
 // (a 128-byte row segment per 8 lanes), transposes in registers and stores V
 // rows y = yg*V + c of V elements along x.
 #define LEGO_V (16 / LEGO_ELEM)
+#ifndef LEGO_MINB
+#define LEGO_MINB 1                   // min CTAs per SM for the register transpose (occupancy knob)
+#endif
 
 static __device__ __forceinline__ unsigned int lego_word(const lego_v16& v, int i) { return v.w[i]; }
 
@@ -315,7 +318,7 @@ LEGO_GLOBAL void __launch_bounds__(256, 2) lego_remap(const unsigned char* __res
     }
 }
 #else
-LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
+LEGO_GLOBAL void __launch_bounds__(256, LEGO_MINB) lego_remap(const unsigned char* __restrict__ src,
                                                    unsigned char* __restrict__ dst,
                                                    long long src_stride, long long dst_stride) {
     // LEGO_TPW warp tiles per warp: every tile's loads are issued before the

@@ -152,7 +152,8 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
                                        smem_bytes=smem)
             src = _assemble(body, {"LEGO_KIND": 2, "LEGO_ELEM": elem_bytes,
                                    "LEGO_SMEM": int(smem_variant), "LEGO_TPW": tpw,
-                                   "LEGO_PERSIST": int(persist), "LEGO_XMAJOR": int(xmajor)})
+                                   "LEGO_PERSIST": int(persist), "LEGO_XMAJOR": int(xmajor),
+                                   "LEGO_MINB": TRANSPOSE_MINB})
             return RemapPlan(runtime.KIND_TRANSPOSE, n_dst, n_src, elem_bytes, False, False, src,
                              info, f"tile {tp.tx}x{tp.ty} {variant}, SX={tp.sx}, DY={tp.dy}")
     width = 1 if masked else lower.contiguous_width(g, f, n_dst, widths=(vec,))
@@ -185,6 +186,8 @@ TRANSPOSE_VARIANT = os.environ.get("LEGO_TRANSPOSE", "")
 # headline transpose and +1.4% on the tiled gather; scripts/quick_hints.py)
 LOAD_HINT = int(os.environ.get("LEGO_LDV", "1"))
 STORE_HINT = int(os.environ.get("LEGO_STV", "0"))
+# minimum resident CTAs per SM requested for the register transpose (register cap)
+TRANSPOSE_MINB = int(os.environ.get("LEGO_TRANSPOSE_MINB", "1"))
 # warp-tile walk order of the transpose ("x", "y" or "block", see lower.transpose_plan)
 TILE_ORDER = os.environ.get("LEGO_TILE_ORDER", "block")
 # CTAs of the persistent transpose variant (2 resident CTAs x 148 SMs by default)
@@ -251,7 +254,7 @@ def _scatter_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
 
 def _remap_program(src_layout, dst_layout, elem_bytes):
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, TRANSPOSE_VARIANT,
-           BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT)
+           BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB)
     plans = []
 
     def build():
