@@ -193,7 +193,11 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, int4* ring_lan
     for (int q = 0; q < RPS; ++q) {
         cur[q] = c.nx1[q];
         c.nx1[q] = c.nx2[q];
+#ifndef NW_ABL_NOLDS
         c.nx2[q] = pf_p[q * (STRIP / 4)];
+#else
+        c.nx2[q] = make_int4(q, lane, s, q ^ lane);
+#endif
         lb[q] = c.bv[q];
     }
     ldsv<RPS>(bnd + (uint32_t)(((RPS * (s + 1)) & (BND_ROWS - 1)) * 4), c.bv);   // next step's boundary
@@ -212,7 +216,9 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, int4* ring_lan
         const int x1 = max(max(cur[q].y + up0 + p2, up1), x0);
         const int x2 = max(max(cur[q].z + up1 + p2, up2), x1);
         const int x3 = max(max(cur[q].w + up2 + p2, up3), x2);
+#ifndef NW_ABL_NOSTS
         if (live) cur_p[q * (STRIP / 4)] = make_int4(x0, x1, x2, x3);   // S' replaces sim in place
+#endif
         up0 = x0; up1 = x1; up2 = x2; up3 = x3;
         d = left[q];
         c.send[q] = live ? x3 : c.send[q];
@@ -224,7 +230,9 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, int4* ring_lan
     c.dprev = live ? d : c.dprev;
     // the strip's last column goes to the right neighbour (lane 31, rows < n)
     const int pub = (lane == 31) & (r0 < n) & live;
+#ifndef NW_ABL_NOPUB
     publish(pub_row, pub, c.send);
+#endif
 }
 
 // one block of STEPS steps (32 rows of lane 0); boundary readiness is checked
