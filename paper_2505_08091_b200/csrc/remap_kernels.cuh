@@ -375,8 +375,14 @@ LEGO_GLOBAL void __launch_bounds__(256, LEGO_MINB) lego_remap(const unsigned cha
 // run to find each diagonal run's base.  LEGO_DIR 0: row-major -> layout
 // (scatter), 1: layout -> row-major (gather).
 typedef lego_elem<LEGO_ELEM>::t lego_e;
-#define BR 64
-#define BK 64
+#ifndef LEGO_BR
+#define LEGO_BR 64
+#endif
+#ifndef LEGO_BK
+#define LEGO_BK 64
+#endif
+#define BR LEGO_BR                                     // rows per band tile (multiple of 32)
+#define BK LEGO_BK                                     // diagonals per band tile (multiple of 32, <= 256)
 // 32-bit index arithmetic: the planner only selects this kernel when n*n < 2^31
 
 LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,

@@ -172,7 +172,11 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
                      f"contiguous={contig}, masked={masked}")
 
 
-BAND_ROWS, BAND_DIAGS = 64, 64
+# band tile (rows x anti-diagonals); static smem BR x (BK+1) elements must stay <= 48 KiB.
+# 0 = measured default per direction (scripts/quick_band.py, 16384^2 int32 on B200):
+# scatter (row-major -> antidiag) 128 x 32, gather 128 x 64
+BAND_ROWS = int(os.environ.get("LEGO_BAND_ROWS", "0"))
+BAND_DIAGS = int(os.environ.get("LEGO_BAND_DIAGS", "0"))
 # transpose kernel variant: "reg" (register micro-tiles, 128-byte src runs,
 # 64-byte dst runs), "regT" (the same with 128-byte dst runs, 64-byte src
 # runs), "reg2" (two tiles per warp in flight), "persist" (persistent,
@@ -207,24 +211,30 @@ def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
     else:
         return None
     n = lower.antidiag_side(side)
-    if n is None or n % BAND_ROWS or n * n >= 2 ** 31 or not lower.diagonal_runs_contiguous(side, n):
+    br = BAND_ROWS or 128
+    bk = BAND_DIAGS or (32 if direction == 0 else 64)
+    if br * (bk + 1) * elem_bytes > 48 * 1024:
+        br, bk = 64, 64
+    if n is not None and n % br:
+        br, bk = 64, 64
+    if n is None or n % br or n * n >= 2 ** 31 or not lower.diagonal_runs_contiguous(side, n):
         return None
     x = lower.flat_var("x", n * n)
     pos = lower.simplify(lower.as_expr(lower.apply_flat(side, x)))
-    kblocks = (n + BAND_ROWS + BAND_DIAGS - 2) // BAND_DIAGS + 1
+    kblocks = (n + br + bk - 2) // bk + 1
     body = codegen.constant("NN", n) + codegen.constant("KBLOCKS", kblocks)
     body += codegen.generate("pos_of", [x], {"p": pos}).source
     order = BAND_ORDER if BAND_ORDER >= 0 else (1 if direction == 0 else 0)
     if order == 0:
-        units = (n // BAND_ROWS) * kblocks
+        units = (n // br) * kblocks
     else:
-        units = ((2 * n - 1 + BAND_DIAGS - 1) // BAND_DIAGS) * (n // BAND_ROWS)
+        units = ((2 * n - 1 + bk - 1) // bk) * (n // br)
     info = runtime.ProgramInfo(kind=runtime.KIND_BAND, elem_bytes=elem_bytes, n=n * n, units=units,
                                unit_threads=256, block=256, smem_bytes=0)
     src = _assemble(body, {"LEGO_KIND": 3, "LEGO_ELEM": elem_bytes, "LEGO_DIR": direction,
-                           "LEGO_BAND_ORDER": order})
+                           "LEGO_BAND_ORDER": order, "LEGO_BR": br, "LEGO_BK": bk})
     return RemapPlan(runtime.KIND_BAND, n * n, n * n, elem_bytes, False, False, src, info,
-                     f"band {BAND_ROWS} rows x {BAND_DIAGS} diagonals, order {order}, "
+                     f"band {br} rows x {bk} diagonals, order {order}, "
                      f"{'scatter' if direction == 0 else 'gather'}")
 
 
@@ -254,7 +264,8 @@ def _scatter_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
 
 def _remap_program(src_layout, dst_layout, elem_bytes):
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, TRANSPOSE_VARIANT,
-           BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB)
+           BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB,
+           BAND_ROWS, BAND_DIAGS)
     plans = []
 
     def build():
