@@ -69,8 +69,14 @@ typedef struct {
     int32_t unit_threads;  /* threads per work unit (1 or 32)                   */
     int32_t block;         /* threads per CTA                                   */
     int32_t smem_bytes;    /* dynamic shared memory per CTA                     */
-    int32_t reserved;
+    int32_t reserved;      /* remap alignment flags: LEGO_ALIGN_SRC_FREE (1) /  */
+                           /* LEGO_ALIGN_DST_FREE (2) = that side's base and    */
+                           /* batch stride need only element alignment; else   */
+                           /* 16 bytes (vector access)                         */
 } lego_program_info;
+
+#define LEGO_ALIGN_SRC_FREE 1
+#define LEGO_ALIGN_DST_FREE 2
 
 int32_t lego_abi_version(void);
 const char *lego_last_error(void);
@@ -111,7 +117,8 @@ lego_status lego_check_bijective(lego_program p, uint32_t *hist, int64_t *violat
 /* For batch b < batch:  dst[b*dst_stride + f] = src[b*src_stride + g(f)]
  * with g = src.apply o dst.inv compiled into the program, i.e. for every
  * logical index x: dst[dst.apply(x)] = src[src.apply(x)].  Strides are in
- * elements; buffers must be 16-byte aligned for the vector paths. */
+ * elements; buffers and batch strides must be 16-byte aligned on the sides
+ * the program accesses with vectors (see lego_program_info.reserved). */
 lego_status lego_remap(lego_program p, const void *src, void *dst, int64_t batch,
                        int64_t src_stride, int64_t dst_stride, void *stream);
 

@@ -321,9 +321,14 @@ extern "C" lego_status lego_remap(lego_program p, const void* src, void* dst, in
     if (!src || !dst) return lego_fail(LEGO_E_ARG, "null buffer");
     if (batch > 65535) return lego_fail(LEGO_E_ARG, "batch above 65535: split the call");
     const int e = p->info.elem_bytes;
-    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    const bool src_vec = !(p->info.reserved & LEGO_ALIGN_SRC_FREE);
+    const bool dst_vec = !(p->info.reserved & LEGO_ALIGN_DST_FREE);
+    const uintptr_t amask = (uintptr_t)(e < 16 ? e - 1 : 15);
+    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & amask)
+        return lego_fail(LEGO_E_ARG, "buffers must be element-aligned");
+    if ((src_vec && (reinterpret_cast<uintptr_t>(src) & 15)) || (dst_vec && (reinterpret_cast<uintptr_t>(dst) & 15)))
         return lego_fail(LEGO_E_ARG, "buffers must be 16-byte aligned");
-    if (batch > 1 && (((src_stride * e) | (dst_stride * e)) & 15))
+    if (batch > 1 && ((src_vec && ((src_stride * e) & 15)) || (dst_vec && ((dst_stride * e) & 15))))
         return lego_fail(LEGO_E_ARG, "batch strides must be multiples of 16 bytes");
     void* args[] = {&src, &dst, &src_stride, &dst_stride};
     return launch(p->remap, (unsigned)p->info.units, (unsigned)batch, (unsigned)p->info.block,

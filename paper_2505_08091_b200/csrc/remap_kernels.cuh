@@ -153,6 +153,25 @@ static __device__ __forceinline__ lego_v16 lego_gather_vec(const unsigned char* 
     return v;
 }
 
+#if LEGO_SCALAR
+// ragged sizes / unaligned batch strides: one element per thread, grid-stride
+LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
+                                                   unsigned char* __restrict__ dst,
+                                                   long long src_stride, long long dst_stride) {
+    const lego_e* s = reinterpret_cast<const lego_e*>(src) + (long long)blockIdx.y * src_stride;
+    lego_e* d = reinterpret_cast<lego_e*>(dst) + (long long)blockIdx.y * dst_stride;
+    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < gen::N;
+         f += (long long)gridDim.x * blockDim.x) {
+        long long si;
+        gen::src_of(f, si);
+#if LEGO_MASKED
+        d[f] = si >= 0 ? s[si] : (lego_e)0;
+#else
+        d[f] = s[si];
+#endif
+    }
+}
+#else
 LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
                                                    unsigned char* __restrict__ dst,
                                                    long long src_stride, long long dst_stride) {
@@ -172,6 +191,7 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
         if (q < nvec) lego_st16(d + q * 16, v[u]);
     }
 }
+#endif  // LEGO_SCALAR
 #endif
 
 // ---------------------------------------------------------------------------
@@ -501,6 +521,20 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
 #define LEGO_VEC (16 / LEGO_ELEM)
 typedef lego_elem<LEGO_ELEM>::t lego_e;
 
+#if LEGO_SCALAR
+LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
+                                                   unsigned char* __restrict__ dst,
+                                                   long long src_stride, long long dst_stride) {
+    const lego_e* s = reinterpret_cast<const lego_e*>(src) + (long long)blockIdx.y * src_stride;
+    lego_e* d = reinterpret_cast<lego_e*>(dst) + (long long)blockIdx.y * dst_stride;
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < gen::N;
+         x += (long long)gridDim.x * blockDim.x) {
+        long long p;
+        gen::pos_of(x, p);
+        if (p >= 0) d[p] = s[x];
+    }
+}
+#else
 LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
                                                    unsigned char* __restrict__ dst,
                                                    long long src_stride, long long dst_stride) {
@@ -517,4 +551,5 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
         if (p >= 0) d[p] = u.e[k];
     }
 }
+#endif  // LEGO_SCALAR
 #endif

@@ -125,8 +125,7 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
     masked = lo < 0
     vec = 16 // elem_bytes
     if n_dst % vec:
-        raise UnsupportedNode(f"destination size {n_dst} is not a multiple of {vec} elements "
-                              f"({elem_bytes}-byte elements, 16-byte vectors)")
+        return _scalar_gather_plan(f, g, n_dst, n_src, elem_bytes, masked)
     if not masked:
         variant = TRANSPOSE_VARIANT or ("smem" if elem_bytes == 1 else "regT")
         smem_variant = variant == "smem"
@@ -158,6 +157,9 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
                              info, f"tile {tp.tx}x{tp.ty} {variant}, SX={tp.sx}, DY={tp.dy}")
     width = 1 if masked else lower.contiguous_width(g, f, n_dst, widths=(vec,))
     contig = width >= vec
+    if contig and (n_src * elem_bytes) % 16:
+        # 16-byte source vectors would straddle batch entries
+        return _scalar_gather_plan(f, g, n_dst, n_src, elem_bytes, masked)
     body = codegen.constant("N", n_dst)
     body += codegen.generate("src_of", [f], {"s": g}).source
     unroll = 4
@@ -165,11 +167,26 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
     nvec = n_dst // vec
     units = (nvec + block * unroll - 1) // (block * unroll)
     info = runtime.ProgramInfo(kind=runtime.KIND_GATHER, elem_bytes=elem_bytes, n=n_dst,
-                               units=units, unit_threads=1, block=block, smem_bytes=0)
+                               units=units, unit_threads=1, block=block, smem_bytes=0,
+                               reserved=0 if contig else runtime.ALIGN_SRC_FREE)
     src = _assemble(body, {"LEGO_KIND": 1, "LEGO_ELEM": elem_bytes, "LEGO_CONTIG": int(contig),
                            "LEGO_MASKED": int(masked), "LEGO_UNROLL": unroll})
     return RemapPlan(runtime.KIND_GATHER, n_dst, n_src, elem_bytes, contig, masked, src, info,
                      f"contiguous={contig}, masked={masked}")
+
+
+def _scalar_gather_plan(f, g, n_dst, n_src, elem_bytes, masked) -> RemapPlan:
+    """Ragged sizes (n_dst not a whole number of 16-byte vectors, or source
+    batch strides that are not 16-byte multiples): one element per thread."""
+    body = codegen.constant("N", n_dst) + codegen.generate("src_of", [f], {"s": g}).source
+    units = max(1, min((n_dst + 255) // 256, 148 * 16))
+    info = runtime.ProgramInfo(kind=runtime.KIND_GATHER, elem_bytes=elem_bytes, n=n_dst,
+                               units=units, unit_threads=1, block=256, smem_bytes=0,
+                               reserved=runtime.ALIGN_SRC_FREE | runtime.ALIGN_DST_FREE)
+    src = _assemble(body, {"LEGO_KIND": 1, "LEGO_ELEM": elem_bytes, "LEGO_SCALAR": 1,
+                           "LEGO_MASKED": int(masked)})
+    return RemapPlan(runtime.KIND_GATHER, n_dst, n_src, elem_bytes, False, masked, src, info,
+                     f"scalar (ragged), masked={masked}")
 
 
 # band tile (rows x anti-diagonals); static smem BR x (BK+1) elements must stay <= 48 KiB.
@@ -230,7 +247,8 @@ def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
     else:
         units = ((2 * n - 1 + bk - 1) // bk) * (n // br)
     info = runtime.ProgramInfo(kind=runtime.KIND_BAND, elem_bytes=elem_bytes, n=n * n, units=units,
-                               unit_threads=256, block=256, smem_bytes=0)
+                               unit_threads=256, block=256, smem_bytes=0,
+                               reserved=runtime.ALIGN_SRC_FREE | runtime.ALIGN_DST_FREE)
     src = _assemble(body, {"LEGO_KIND": 3, "LEGO_ELEM": elem_bytes, "LEGO_DIR": direction,
                            "LEGO_BAND_ORDER": order, "LEGO_BR": br, "LEGO_BK": bk})
     return RemapPlan(runtime.KIND_BAND, n * n, n * n, elem_bytes, False, False, src, info,
@@ -250,14 +268,14 @@ def _scatter_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
     x, app = lower.apply_map_expr(dst_layout)
     n_src = lower.logical_size(dst_layout)
     vec = 16 // elem_bytes
-    if n_src % vec:
-        raise UnsupportedNode(f"source size {n_src} is not a multiple of {vec} elements")
+    scalar = n_src % vec != 0                               # ragged: one element per thread
     n_dst = lower.value_range(app)[1] + 1                   # highest position + 1
     body = codegen.constant("N", n_src) + codegen.generate("pos_of", [x], {"p": app}).source
+    units = max(1, min((n_src + 255) // 256, 148 * 16)) if scalar else (n_src // vec + 255) // 256
     info = runtime.ProgramInfo(kind=runtime.KIND_SCATTER, elem_bytes=elem_bytes, n=n_src,
-                               units=(n_src // vec + 255) // 256, unit_threads=1, block=256,
-                               smem_bytes=0)
-    src = _assemble(body, {"LEGO_KIND": 4, "LEGO_ELEM": elem_bytes})
+                               units=units, unit_threads=1, block=256, smem_bytes=0,
+                               reserved=runtime.ALIGN_DST_FREE | (runtime.ALIGN_SRC_FREE if scalar else 0))
+    src = _assemble(body, {"LEGO_KIND": 4, "LEGO_ELEM": elem_bytes, "LEGO_SCALAR": int(scalar)})
     return RemapPlan(runtime.KIND_SCATTER, n_dst, n_src, elem_bytes, False, False, src, info,
                      f"scatter into an injective layout, {n_dst} positions")
 

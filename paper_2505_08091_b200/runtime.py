@@ -50,6 +50,8 @@ class ProgramInfo(ctypes.Structure):
 
 
 KIND_INDEX_MAP, KIND_GATHER, KIND_TRANSPOSE, KIND_BAND, KIND_SCATTER = 0, 1, 2, 3, 4
+# lego_program_info.reserved flags (include/lego_b200.h): element-aligned buffers suffice
+ALIGN_SRC_FREE, ALIGN_DST_FREE = 1, 2
 
 _lib = None
 _lock = threading.Lock()

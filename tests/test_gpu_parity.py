@@ -101,10 +101,7 @@ def test_scatter_gather_vs_oracle(name, dtype):
     if c["spec"]["kind"] == "expand":
         pytest.skip("ExpandBy remaps are covered by test_expand_remap")
     dt = getattr(torch, dtype)
-    vec = 16 // torch.tensor([], dtype=dt).element_size()
-    if c["size"] % vec:
-        pytest.skip("size not a multiple of the 16-byte vector")
-    g = _layout(c)
+    g = _layout(c)                 # ragged sizes take the scalar gather / scatter kernels
     _check_remap(None, c["spec"], None, g, dt, batch=2)
     _check_remap(c["spec"], None, g, None, dt, batch=1)
 
