@@ -123,7 +123,9 @@ lego_status lego_remap(lego_program p, const void *src, void *dst, int64_t batch
                        int64_t src_stride, int64_t dst_stride, void *stream);
 
 /* --- fixed kernels with LEGO-derived layouts ------------------------------ */
-/* Row softmax, fp32, rows x cols row-major (cols % 4 == 0). */
+/* Row softmax, fp32, rows x cols row-major.  Rows in registers with float4
+ * access when cols % 4 == 0 and both buffers are 16-byte aligned; any other
+ * shape takes a scalar two-pass kernel (4-byte alignment). */
 lego_status lego_softmax_f32(const float *x, float *y, int64_t rows, int64_t cols, void *stream);
 
 /* Needleman-Wunsch score matrix: score is (n+1) x (n+1) int32, row-major;

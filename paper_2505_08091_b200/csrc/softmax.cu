@@ -123,17 +123,41 @@ __global__ void __launch_bounds__(kThreads) softmax_rows_stream(const float* __r
     }
 }
 
+// any row length / 4-byte alignment: scalar accesses, online (max, sum), then normalise
+__global__ void __launch_bounds__(kThreads) softmax_rows_scalar(const float* __restrict__ x,
+                                                                float* __restrict__ y, long long cols) {
+    __shared__ float red[kThreads / 32];
+    const float* xr = x + (long long)blockIdx.x * cols;
+    float* yr = y + (long long)blockIdx.x * cols;
+    float m = -INFINITY, s = 0.f;
+    for (long long k = threadIdx.x; k < cols; k += kThreads) {
+        const float v = xr[k];
+        const float nm = fmaxf(m, v);
+        s = s * exp2f((m - nm) * kLog2e) + exp2f((v - nm) * kLog2e);
+        m = nm;
+    }
+    const float gm = block_reduce<true>(m, red);
+    s = m == -INFINITY ? 0.f : s * exp2f((m - gm) * kLog2e);
+    const float inv = 1.f / block_reduce<false>(s, red);
+    const float mb = gm * kLog2e;
+    for (long long k = threadIdx.x; k < cols; k += kThreads) yr[k] = exp2f(fmaf(xr[k], kLog2e, -mb)) * inv;
+}
+
 }  // namespace
 
 extern "C" lego_status lego_softmax_f32(const float* x, float* y, int64_t rows, int64_t cols,
                                         void* stream) {
     if (rows < 0 || cols <= 0) return lego_fail(LEGO_E_SHAPE, "bad softmax shape %lld x %lld",
                                                 (long long)rows, (long long)cols);
-    if (cols % 4) return lego_fail(LEGO_E_SHAPE, "softmax needs cols %% 4 == 0 (got %lld)", (long long)cols);
-    if (((uintptr_t)x | (uintptr_t)y) & 15) return lego_fail(LEGO_E_ARG, "buffers must be 16-byte aligned");
+    if (!x || !y) return lego_fail(LEGO_E_ARG, "null buffer");
+    if (((uintptr_t)x | (uintptr_t)y) & 3) return lego_fail(LEGO_E_ARG, "buffers must be 4-byte aligned");
     if (rows == 0) return LEGO_OK;
     if (rows > 0x7fffffffLL) return lego_fail(LEGO_E_SHAPE, "too many rows");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cols % 4 || (((uintptr_t)x | (uintptr_t)y) & 15)) {   // ragged rows: scalar path
+        softmax_rows_scalar<<<(unsigned)rows, kThreads, 0, st>>>(x, y, cols);
+        return lego_cuda_check(cudaGetLastError(), "softmax launch");
+    }
     const long long per_pass = 4LL * kThreads;                  // floats per register "it"
     const long long its = (cols + per_pass - 1) / per_pass;
     dim3 grid((unsigned)rows);

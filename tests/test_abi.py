@@ -42,7 +42,9 @@ def test_null_arguments_fail_cleanly():
     st = lib.lego_remap(None, None, None, 1, 0, 0, None)
     assert st == 8 and b"not a remap program" in lib.lego_last_error()
     st = lib.lego_softmax_f32(None, None, 4, 3, None)
-    assert st == 3 and b"cols % 4" in lib.lego_last_error()
+    assert st == 8 and b"null buffer" in lib.lego_last_error()
+    st = lib.lego_softmax_f32(None, None, 4, 0, None)
+    assert st == 3 and b"bad softmax shape" in lib.lego_last_error()
     with pytest.raises(L.ShapeMismatch):
         R.check(lib.lego_gemm_bf16(None, None, None, 100, 256, 64, 1, 1, None))
     # NW: argument checks run before any CUDA call (offset-score range, alignment)

@@ -40,6 +40,17 @@ def test_gemm_8192_cubed():
     _gemm_check(8192, 8192, 8192)
 
 
+@pytest.mark.parametrize("rows,cols", [(3, 1), (5, 7), (17, 1023), (2, 4097), (4, 300001)])
+def test_softmax_ragged_rows(rows, cols):
+    """cols % 4 != 0 takes the scalar kernel (max-rel <= 1e-5 vs float64)."""
+    g = torch.Generator(device="cuda").manual_seed(cols)
+    x = torch.randn(rows, cols, device="cuda", generator=g) * 4
+    y = K.softmax(x)
+    ref = torch.softmax(x.double(), dim=-1)
+    rel = ((y.double() - ref).abs() / ref.abs().clamp_min(1e-30)).max().item()
+    assert rel <= 1e-5, rel
+
+
 def test_gemm_rejects_bad_shapes():
     import paper_2505_08091_b200 as L
     a = torch.zeros(100, 64, device="cuda", dtype=torch.bfloat16)
