@@ -144,10 +144,13 @@ lego_status lego_nw_i32(const int32_t *sim, int32_t *score, int64_t n, int32_t p
  * A is M x K row-major, B is N x K row-major ("TN"), C is M x N row-major
  * bf16, fp32 accumulation.  raster: 0 = row-major CTA order, G > 0 = the
  * LEGO grouped raster GroupBy([MB/G, NB, G]).OrderBy(Row(MB/G, NB, G)) over
- * output tiles (G m-blocks of 128 rows per group).  Requires M % 128 == 0,
- * N % 256 == 0, K % 64 == 0.  When M % 256 == 0 the CTA-pair kernel runs
- * (cta_group::2, 256 x 256 tiles per 2-SM cluster; LEGO_GEMM_PAIR=0 disables
- * it), otherwise the single-CTA 128 x 256 kernel. */
+ * output tiles (G m-blocks of 128 rows per group).  Requires N % 8 == 0 and
+ * K % 8 == 0 (16-byte rows); M, N, K need not be tile multiples (TMA
+ * zero-fills the operand tails, the epilogue masks the stores).  The CTA-pair
+ * kernel (cta_group::2, 256 x 512 or 256 x 256 tiles per 2-SM cluster) runs
+ * for M % 256 == 0 and for ragged shapes; M % 256 == 128 with exact N, K
+ * tiles takes the single-CTA 128 x 256 kernel (LEGO_GEMM_PAIR=0 forces it
+ * for all exact shapes). */
 lego_status lego_gemm_bf16(const void *A, const void *B, void *C, int64_t M, int64_t N,
                            int64_t K, int64_t batch, int32_t raster, void *stream);
 

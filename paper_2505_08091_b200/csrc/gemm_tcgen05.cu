@@ -419,9 +419,12 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
-    const int kblocks = K / BK;
-    // tiles are 256 x 256 output blocks: "m-blocks" of 256 rows
-    Raster ras{M / (2 * BM), N / BN, (M / (2 * BM)) * (N / BN), raster_mode > 0 ? raster_mode : 1};
+    // ragged shapes: the last k-block / tile rows / tile columns run past K, M, N;
+    // TMA zero-fills the operand boxes there and the epilogue masks the stores
+    const int kblocks = (K + BK - 1) / BK;
+    const int mtiles = (M + 2 * BM - 1) / (2 * BM), ntiles = (N + BN - 1) / BN;
+    // tiles are 256-row "m-blocks" x BN columns
+    Raster ras{mtiles, ntiles, mtiles * ntiles, raster_mode > 0 ? raster_mode : 1};
     const int total_tiles = ras.per_batch * batch;
     const int pair_id = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
 
@@ -582,7 +585,9 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
                     for (int q = 0; q < 4; ++q) {
                         const int r = 8 * q + (lane >> 2), cq = lane & 3;
                         const uint4 o = *reinterpret_cast<const uint4*>(stg + r * 64 + 16 * (cq ^ ((r >> 1) & 3)));
-                        *reinterpret_cast<uint4*>(cbase + static_cast<size_t>(r) * N + c + 32 * h2 + 8 * cq) = o;
+                        const int gcol = nb * BN + half * EPI_COLS + c + 32 * h2 + 8 * cq;   // N % 8 == 0
+                        if (row0 + r < M && gcol < N)
+                            *reinterpret_cast<uint4*>(cbase + static_cast<size_t>(r) * N + c + 32 * h2 + 8 * cq) = o;
                     }
                     __syncwarp();
                 }
@@ -665,9 +670,11 @@ extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int
                                       int64_t batch, int32_t raster, void* stream) {
     if (M <= 0 || N <= 0 || K <= 0 || batch <= 0)
         return lego_fail(LEGO_E_SHAPE, "gemm shape must be positive");
-    if (M % BM || N % BN || K % BK)
-        return lego_fail(LEGO_E_SHAPE, "gemm needs M %% %d == 0, N %% %d == 0, K %% %d == 0 (got %lld %lld %lld)",
-                         BM, BN, BK, (long long)M, (long long)N, (long long)K);
+    if (N % 8 || K % 8)
+        return lego_fail(LEGO_E_SHAPE, "gemm needs N %% 8 == 0 and K %% 8 == 0 (16-byte rows; got N=%lld K=%lld)",
+                         (long long)N, (long long)K);
+    // exact tiles: single-CTA 128 x 256 when M % 256 != 0; anything ragged goes to the pair kernel
+    const bool ragged = M % BM || N % BN || K % BK;
     if (M * batch > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
         return lego_fail(LEGO_E_SHAPE, "gemm dimensions too large");
     if (((uintptr_t)A | (uintptr_t)B | (uintptr_t)C) & 15)
@@ -679,13 +686,14 @@ extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int
         const char* e = getenv("LEGO_GEMM_PAIR");
         return !(e && e[0] == '0');
     }();
-    if (pair_ok && M % (2 * pair::BM) == 0 && N % pair::BN == 0) {
+    if (ragged || (pair_ok && M % (2 * pair::BM) == 0 && N % pair::BN == 0)) {
         // CTA-pair kernel on cta_group::2: 256 x 512 tiles when N allows, else 256 x 256
-        const bool wide = N % 512 == 0 && pair_wide();
+        const bool wide = (ragged ? N > 256 : N % 512 == 0) && pair_wide();
         CUtensorMap ma, mb;
         LEGO_TRY(make_map(&ma, A, M, K, batch, pair::BM));
         LEGO_TRY(make_map(&mb, B, N, K, batch, 128));
-        const int64_t tiles = (M / (2 * pair::BM)) * (N / (wide ? 512 : 256)) * batch;
+        const int64_t tn = wide ? 512 : 256;
+        const int64_t tiles = ((M + 255) / 256) * ((N + tn - 1) / tn) * batch;
         const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
         const int g = raster > 1 ? raster / 2 : raster;   // G counts 128-row m-blocks; pair tiles are 256 rows
         if (wide) return launch_pair<2>(ma, mb, C, M, N, K, batch, g, pairs, stream);

@@ -36,6 +36,13 @@ def test_gemm_small_shapes():
     _gemm_check(1024, 1280, 192, batch=2)       # pair, 256x256 (N % 512 = 256)
 
 
+@pytest.mark.parametrize("M,N,Kd,batch", [(8, 8, 8, 1), (100, 72, 40, 1), (257, 520, 136, 2),
+                                          (1000, 1000, 1000, 1), (130, 264, 72, 3)])
+def test_gemm_ragged_shapes(M, N, Kd, batch):
+    # tails: TMA zero-fills operand boxes past M, N, K; the epilogue masks rows >= M, cols >= N
+    _gemm_check(M, N, Kd, batch=batch)
+
+
 def test_gemm_8192_cubed():
     _gemm_check(8192, 8192, 8192)
 
@@ -53,7 +60,7 @@ def test_softmax_ragged_rows(rows, cols):
 
 def test_gemm_rejects_bad_shapes():
     import paper_2505_08091_b200 as L
-    a = torch.zeros(100, 64, device="cuda", dtype=torch.bfloat16)
+    a = torch.zeros(100, 60, device="cuda", dtype=torch.bfloat16)      # K % 8 != 0
     with pytest.raises(L.ShapeMismatch):
         K.gemm(a, a)
 
