@@ -149,9 +149,9 @@ extern "C" lego_status lego_softmax_f32(const float* x, float* y, int64_t rows, 
                                         void* stream) {
     if (rows < 0 || cols <= 0) return lego_fail(LEGO_E_SHAPE, "bad softmax shape %lld x %lld",
                                                 (long long)rows, (long long)cols);
+    if (rows == 0) return LEGO_OK;
     if (!x || !y) return lego_fail(LEGO_E_ARG, "null buffer");
     if (((uintptr_t)x | (uintptr_t)y) & 3) return lego_fail(LEGO_E_ARG, "buffers must be 4-byte aligned");
-    if (rows == 0) return LEGO_OK;
     if (rows > 0x7fffffffLL) return lego_fail(LEGO_E_SHAPE, "too many rows");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (cols % 4 || (((uintptr_t)x | (uintptr_t)y) & 15)) {   // ragged rows: scalar path

@@ -544,7 +544,7 @@ extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n
     if (n < 0 || batch < 0) return lego_fail(LEGO_E_SHAPE, "negative NW size");
     if (batch == 0) return LEGO_OK;
     if (n > (1 << 20)) return lego_fail(LEGO_E_SHAPE, "NW n above 2^20");
-    if (!sim || !score) return lego_fail(LEGO_E_ARG, "null buffer");
+    if (!score || (n > 0 && !sim)) return lego_fail(LEGO_E_ARG, "null buffer");
     if ((uintptr_t)sim & 15) return lego_fail(LEGO_E_ARG, "sim must be 16-byte aligned");
     if ((long long)std::llabs((long long)penalty) * (2 * n + 2) >= (1LL << 30))
         return lego_fail(LEGO_E_ARG, "|penalty| * (2n + 2) must stay below 2^30 (offset scores are int32)");

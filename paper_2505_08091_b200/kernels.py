@@ -442,7 +442,9 @@ def nw_score(sim, penalty: int, *, out=None, stream=None):
         raise ShapeMismatch("nw_score takes a CUDA int32 tensor of shape (..., n, n)")
     sim = sim.contiguous()
     n = sim.shape[-1]
-    batch = sim.numel() // (n * n) if n else 0
+    batch = 1
+    for d in sim.shape[:-2]:
+        batch *= d
     if out is None:
         out = torch.empty(*sim.shape[:-2], n + 1, n + 1, dtype=torch.int32, device=sim.device)
     runtime.check(runtime.lib().lego_nw_i32(sim.data_ptr(), out.data_ptr(), n, int(penalty), batch,
@@ -469,9 +471,15 @@ def gemm(a, b, *, out=None, raster: Optional[int] = None, stream=None):
     N = b.shape[-2]
     if b.shape[-1] != K:
         raise ShapeMismatch(f"inner dims differ: {K} vs {b.shape[-1]}")
-    batch = a.numel() // (M * K)
+    batch = 1
+    for d in a.shape[:-2]:
+        batch *= d
     if out is None:
         out = torch.empty(*a.shape[:-2], M, N, dtype=torch.bfloat16, device=a.device)
+    if batch == 0 or M == 0 or N == 0:
+        return out
+    if K == 0:
+        return out.zero_()
     runtime.check(runtime.lib().lego_gemm_bf16(a.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K,
                                                batch, raster, runtime.stream_handle(stream)),
                   "lego_gemm_bf16")

@@ -80,3 +80,19 @@ def test_nw_16384():
     sim = rng.integers(-10, 11, size=(n, n), dtype=np.int32)
     got = K.nw_score(torch.from_numpy(sim).cuda(), 10).cpu().numpy()
     np.testing.assert_array_equal(got, O.nw(sim, 10))
+
+
+def test_empty_inputs():
+    """Empty batches and zero-size problems return empty results without launching."""
+    import paper_2505_08091_b200 as L
+    g = L.parse_layout("GroupBy([64,64]).OrderBy(Col(64,64))")
+    x = torch.empty(0, 64 * 64, device="cuda", dtype=torch.float32)
+    assert K.remap(x, None, g).shape == (0, 64 * 64)
+    assert K.softmax(torch.empty(0, 8, device="cuda")).shape == (0, 8)
+    s = K.nw_score(torch.empty(0, 5, 5, device="cuda", dtype=torch.int32), 10)
+    assert s.shape == (0, 6, 6)
+    s = K.nw_score(torch.empty(0, 0, device="cuda", dtype=torch.int32), 10)
+    assert s.shape == (1, 1) and s.item() == 0
+    c = K.gemm(torch.empty(0, 128, 64, device="cuda", dtype=torch.bfloat16),
+               torch.empty(0, 256, 64, device="cuda", dtype=torch.bfloat16))
+    assert c.shape == (0, 128, 256)
