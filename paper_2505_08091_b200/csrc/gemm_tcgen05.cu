@@ -547,6 +547,10 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
         const int quarter = warp & 3;
         const int half = (warp - 2) >> 2;
         constexpr int EPI_COLS = 256;                         // columns per epilogue warp
+#ifndef LEGO_GEMM_EPI_CHUNKS
+#define LEGO_GEMM_EPI_CHUNKS 2
+#endif
+        constexpr int EPI_CHUNKS = LEGO_GEMM_EPI_CHUNKS;      // 32-column TMEM loads in flight
         int it = 0;
         for (int t = pair_id; t < total_tiles; t += num_pairs, ++it) {
             int b, mb, nb;
@@ -563,13 +567,16 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
             const uint32_t taddr = tmem_base + acc * ACC_COLS + half * EPI_COLS +
                                    (static_cast<uint32_t>(quarter * 32) << 16);
 #pragma unroll 1
-            for (int c = 0; c < EPI_COLS; c += 64) {
-                uint32_t v[2][32];                              // two chunks per TMEM round trip
-                tmem_ld32(taddr + c, v[0]);
-                tmem_ld32(taddr + c + 32, v[1]);
+#ifdef LEGO_GEMM_ABL_NOEPI
+            if (M < 0)                                          // ablation: skip the epilogue body
+#endif
+            for (int c = 0; c < EPI_COLS; c += 32 * EPI_CHUNKS) {
+                uint32_t v[EPI_CHUNKS][32];                     // EPI_CHUNKS x 32 columns per TMEM round trip
+#pragma unroll
+                for (int h2 = 0; h2 < EPI_CHUNKS; ++h2) tmem_ld32(taddr + c + 32 * h2, v[h2]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
+                for (int h2 = 0; h2 < EPI_CHUNKS; ++h2) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         uint4 o;
