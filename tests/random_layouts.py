@@ -1,0 +1,67 @@
+"""Seeded generator of random LEGO layout DSL strings (tiled GroupBy + 1-2
+OrderBy stages of RegP / Row / Col / GenP(antidiag | rev2d) perms), used by the
+CPU frontend-vs-oracle test and the GPU parity test.  Sizes stay <= 8192."""
+
+import random
+
+
+def _factor(n, rng):
+    ds = [d for d in range(2, n) if n % d == 0]
+    if not ds:
+        return None
+    a = rng.choice(ds)
+    return a, n // a
+
+
+def _perm(dims, rng):
+    """One perm over exactly `dims` (a list of extents)."""
+    k = len(dims)
+    choice = rng.random()
+    if k == 2 and dims[0] == dims[1] and choice < 0.3:
+        return f"GenP([{dims[0]},{dims[1]}], {rng.choice(['antidiag', 'rev2d'])})"
+    if choice < 0.5:
+        sigma = list(range(1, k + 1))
+        rng.shuffle(sigma)
+        return f"RegP([{','.join(map(str, dims))}],[{','.join(map(str, sigma))}])"
+    if choice < 0.75:
+        return f"Row({','.join(map(str, dims))})"
+    return f"Col({','.join(map(str, dims[::-1]))})"      # Col takes memory-order extents
+
+
+def random_layout(rng):
+    d = rng.choice([1, 2, 2, 2, 3])
+    while True:
+        ext = [rng.choice([2, 3, 4, 5, 6, 8, 9, 12, 16, 24, 32]) for _ in range(d)]
+        size = 1
+        for e in ext:
+            size *= e
+        if 4 <= size <= 8192:
+            break
+    # optional tiling: split each extent into outer x inner
+    tiles = [ext]
+    if rng.random() < 0.6:
+        outer, inner = [], []
+        for e in ext:
+            f = _factor(e, rng)
+            if f is None:
+                outer.append(1)
+                inner.append(e)
+            else:
+                outer.append(f[0])
+                inner.append(f[1])
+        if all(o > 1 for o in outer):
+            tiles = [outer, inner]
+    dims = [n for t in tiles for n in t]
+    text = "GroupBy(" + ", ".join("[" + ",".join(map(str, t)) + "]" for t in tiles) + ")"
+    for _ in range(rng.choice([1, 1, 2])):
+        if len(dims) >= 2 and rng.random() < 0.5:
+            cut = rng.randrange(1, len(dims))
+            text += f".OrderBy({_perm(dims[:cut], rng)}, {_perm(dims[cut:], rng)})"
+        else:
+            text += f".OrderBy({_perm(dims, rng)})"
+    return text
+
+
+def corpus(count=60, seed=20261017):
+    rng = random.Random(seed)
+    return [random_layout(rng) for _ in range(count)]
