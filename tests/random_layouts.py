@@ -65,3 +65,24 @@ def random_layout(rng):
 def corpus(count=60, seed=20261017):
     rng = random.Random(seed)
     return [random_layout(rng) for _ in range(count)]
+
+
+def random_expand(rng):
+    """ExpandBy(physical, expanded, inner): partial tiles of a random tiled layout."""
+    while True:
+        inner = random_layout(rng)
+        if not inner.startswith("GroupBy("):
+            continue
+        import re
+        tiles = [list(map(int, t.split(","))) for t in re.findall(r"\[([0-9,]+)\]", inner.split(".")[0])]
+        k = len(tiles[0])
+        expanded = [1] * k
+        for t in tiles:
+            expanded = [a * b for a, b in zip(expanded, t)]
+        physical = [max(1, e - rng.randrange(0, max(1, e // 3) + 1)) for e in expanded]
+        return (f"ExpandBy([{','.join(map(str, physical))}],[{','.join(map(str, expanded))}],{inner})")
+
+
+def expand_corpus(count=24, seed=20261018):
+    rng = random.Random(seed)
+    return [random_expand(rng) for _ in range(count)]

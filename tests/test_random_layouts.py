@@ -46,3 +46,32 @@ def test_device_maps_and_remaps_match_oracle(text):
         for b in range(2):
             assert np.array_equal(fwd[b], O.remap(host[b], None, spec)), (text, dt)
             assert np.array_equal(back[b], O.remap(host[b], spec, None)), (text, dt)
+
+
+EXPAND = __import__("random_layouts").expand_corpus()
+
+
+@pytest.mark.parametrize("text", EXPAND[::3])
+def test_frontend_expand_matches_oracle(text):
+    g = L.parse_layout(text)
+    spec = O.parse(text)
+    dims = O.dims(spec)
+    app = O.apply_range(spec)
+    for x in range(O.logical_size(spec)):
+        got = g.apply(tuple(int(v) for v in np.unravel_index(x, dims)))
+        assert (-1 if got is None else got) == app[x]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("text", EXPAND)
+def test_device_expand_maps_and_gather_match_oracle(text):
+    torch = pytest.importorskip("torch")
+    from paper_2505_08091_b200 import kernels as K
+    g = L.parse_layout(text)
+    spec = O.parse(text)
+    assert np.array_equal(K.apply_map(g).cpu().numpy(), O.apply_range(spec))
+    assert np.array_equal(K.inv_map(g).cpu().numpy(), O.inv_range(spec))
+    # gather: physical (partial-tile) buffer -> logical row-major, masked slots read 0
+    host = np.arange(O.size(spec), dtype=np.int32) + 1
+    got = K.remap(torch.from_numpy(host).cuda(), g, None).cpu().numpy()
+    assert np.array_equal(got, O.remap(host, spec, None, dst_size=O.logical_size(spec)))
