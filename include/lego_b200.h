@@ -154,6 +154,16 @@ lego_status lego_nw_i32(const int32_t *sim, int32_t *score, int64_t n, int32_t p
 lego_status lego_gemm_bf16(const void *A, const void *B, void *C, int64_t M, int64_t N,
                            int64_t K, int64_t batch, int32_t raster, void *stream);
 
+/* The four data-layout variants of the paper's LEGO matmul (Row vs Col
+ * layouts of each operand): a_major / b_major = 0 keeps
+ * the operand K-major (A: M x K, B: N x K row-major, as above), 1 makes it
+ * MN-major (A stored K x M, B stored K x N row-major), fed to tcgen05 as an
+ * MN-major UMMA operand (no transpose pass).  MN-major A needs M % 8 == 0;
+ * K % 8 == 0 is needed only while an operand is K-major. */
+lego_status lego_gemm_bf16_ex(const void *A, const void *B, void *C, int64_t M, int64_t N,
+                              int64_t K, int64_t batch, int32_t raster, int32_t a_major,
+                              int32_t b_major, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

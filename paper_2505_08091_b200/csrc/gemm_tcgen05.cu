@@ -115,6 +115,20 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
     return d;
 }
 
+// UMMA shared-memory descriptor: MN-major, SWIZZLE_128B.  Canonical layout
+// (in 16-byte units) ((8,n),(8,k)):((1,LBO),(8,SBO)): 64 MN-elements x 8 k-rows
+// per 1024-byte atom, k-row groups SBO = 1024 B apart, 64-element MN groups
+// LBO = 8 KiB apart (one 64 x 64 TMA box per MN group).
+__device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr & 0x3FFFF) >> 4);         // start address        [0,14)
+    d |= static_cast<uint64_t>(8192 >> 4) << 16;                // LBO = 8 KiB          [16,30)
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;                // SBO = 1024 B         [32,46)
+    d |= static_cast<uint64_t>(1) << 46;                        // version = 1 (sm100)  [46,48)
+    d |= static_cast<uint64_t>(2) << 61;                        // SWIZZLE_128B         [61,64)
+    return d;
+}
+
 // instruction descriptor: kind::f16, A/B bf16 K-major, D fp32, M=128, N=256
 __host__ __device__ constexpr uint32_t make_idesc() {
     return (1u << 4)                       // D format F32
@@ -395,7 +409,9 @@ __host__ __device__ constexpr uint32_t make_idesc2() {
     return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(256 >> 3) << 17) | (uint32_t(256 >> 4) << 24);
 }
 
-template <int NH>
+// operand majors: TA / TB = the operand is stored MN-major ("Col" data layout:
+// A as K x M, B as K x N row-major), else K-major (A as M x K, B as N x K)
+template <int NH, bool TA, bool TB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NH>::NUM_THREADS, 1)
 gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                        __nv_bfloat16* __restrict__ C, int M, int N, int K, int batch, int raster_mode) {
@@ -472,12 +488,24 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     if (leader) mbar_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
                     const uint32_t fb = full_leader + 8u * stage;
-                    tma_load_3d_pair(sA + stage * A_BYTES, &tmap_a, fb, kb * BK, arow, b);
+                    if (TA) {                                   // two 64(M) x 64(K) boxes
+                        tma_load_3d_pair(sA + stage * A_BYTES, &tmap_a, fb, arow, kb * BK, b);
+                        tma_load_3d_pair(sA + stage * A_BYTES + 8192, &tmap_a, fb, arow + 64, kb * BK, b);
+                    } else {
+                        tma_load_3d_pair(sA + stage * A_BYTES, &tmap_a, fb, kb * BK, arow, b);
+                    }
                     // B half h: this CTA's 128 rows of the output columns [256h, 256h + 256)
 #pragma unroll
-                    for (int h = 0; h < NH; ++h)
-                        tma_load_3d_pair(sB + stage * B_BYTES + h * (128 * BK * 2), &tmap_b, fb, kb * BK,
-                                         nb * BN + h * 256 + (int)rank * 128, b);
+                    for (int h = 0; h < NH; ++h) {
+                        const int brow = nb * BN + h * 256 + (int)rank * 128;
+                        unsigned char* dstb = sB + stage * B_BYTES + h * (128 * BK * 2);
+                        if (TB) {
+                            tma_load_3d_pair(dstb, &tmap_b, fb, brow, kb * BK, b);
+                            tma_load_3d_pair(dstb + 8192, &tmap_b, fb, brow + 64, kb * BK, b);
+                        } else {
+                            tma_load_3d_pair(dstb, &tmap_b, fb, kb * BK, brow, b);
+                        }
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -485,7 +513,14 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA only) =====================
         if (leader) {
-            constexpr uint32_t idesc = make_idesc2();
+            constexpr uint32_t idesc = make_idesc2() | (uint32_t(TA) << 15) | (uint32_t(TB) << 16);
+            // K step k (16 elements): +32 B inside the K-major swizzle row, or +2 atoms (2 x 8 k-rows)
+            auto adesc = [](uint32_t base, int k) {
+                return TA ? smem_desc_mn(base + k * 2048) : smem_desc(base + k * UMMA_K * 2);
+            };
+            auto bdesc = [](uint32_t base, int k) {
+                return TB ? smem_desc_mn(base + k * 2048) : smem_desc(base + k * UMMA_K * 2);
+            };
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -506,8 +541,7 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < BK / UMMA_K; ++k)
-                                tc_mma2(d_tmem, smem_desc(a0 + k * UMMA_K * 2), smem_desc(b0 + k * UMMA_K * 2), idesc,
-                                        k != 0);
+                                tc_mma2(d_tmem, adesc(a0, k), bdesc(b0, k), idesc, k != 0);
                         }
                         __syncwarp();
                         mbar_wait(&acc_empty[1], acc_phase ^ 1);
@@ -515,8 +549,7 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
                         if (elect_one()) {
 #pragma unroll
                             for (int k = 0; k < BK / UMMA_K; ++k)
-                                tc_mma2(d_tmem + 256, smem_desc(a0 + k * UMMA_K * 2),
-                                        smem_desc(b0 + 128 * BK * 2 + k * UMMA_K * 2), idesc, k != 0);
+                                tc_mma2(d_tmem + 256, adesc(a0, k), bdesc(b0 + 128 * BK * 2, k), idesc, k != 0);
                             tc_commit2(&empty_bar[stage]);
                             if (kb == kblocks - 1) tc_commit2(&acc_full[acc]);
                         }
@@ -531,8 +564,8 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
                         for (int k = 0; k < BK / UMMA_K; ++k)
 #pragma unroll
                             for (int h = 0; h < NH; ++h)
-                                tc_mma2(d_tmem + h * 256, smem_desc(a0 + k * UMMA_K * 2),
-                                        smem_desc(b0 + h * (128 * BK * 2) + k * UMMA_K * 2), idesc, (kb | k) != 0);
+                                tc_mma2(d_tmem + h * 256, adesc(a0, k), bdesc(b0 + h * (128 * BK * 2), k), idesc,
+                                        (kb | k) != 0);
                         tc_commit2(&empty_bar[stage]);
                         if (kb == kblocks - 1) tc_commit2(&acc_full[acc]);
                     }
@@ -632,6 +665,21 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
+// MN-major operand stored K x rows row-major (rows contiguous): box = 64 rows x 64 k
+lego_status make_map_mn(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t batch) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return lego_fail(LEGO_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)K, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)rows * 2, (cuuint64_t)(rows * K * 2)};
+    cuuint32_t box[3] = {64, BK, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return lego_fail(LEGO_E_CUDA, "cuTensorMapEncodeTiled (MN-major) failed (%d)", (int)r);
+    return LEGO_OK;
+}
+
 lego_status make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t batch, int box_rows) {
     EncodeTiledFn enc = encode_fn();
     if (!enc) return lego_fail(LEGO_E_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -646,19 +694,19 @@ lego_status make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K
     return LEGO_OK;
 }
 
-template <int NH>
+template <int NH, bool TA, bool TB>
 lego_status launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t M, int64_t N, int64_t K,
                         int64_t batch, int raster, int64_t pairs, void* stream) {
     using C_ = pair::Cfg<NH>;
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(pair::gemm_bf16_tcgen05_pair<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   C_::SMEM_BYTES);
+        err = cudaFuncSetAttribute(pair::gemm_bf16_tcgen05_pair<NH, TA, TB>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES);
     });
     LEGO_TRY(lego_cuda_check(err, "cudaFuncSetAttribute(gemm pair smem)"));
-    pair::gemm_bf16_tcgen05_pair<NH><<<(unsigned)(2 * pairs), C_::NUM_THREADS, C_::SMEM_BYTES,
-                                       static_cast<cudaStream_t>(stream)>>>(
+    pair::gemm_bf16_tcgen05_pair<NH, TA, TB><<<(unsigned)(2 * pairs), C_::NUM_THREADS, C_::SMEM_BYTES,
+                                               static_cast<cudaStream_t>(stream)>>>(
         ma, mb, static_cast<__nv_bfloat16*>(C), (int)M, (int)N, (int)K, (int)batch, raster);
     return lego_cuda_check(cudaGetLastError(), "gemm pair launch");
 }
@@ -671,17 +719,27 @@ bool pair_wide() {
     return w;
 }
 
-}  // namespace
+template <int NH>
+lego_status dispatch_pair(bool ta, bool tb, const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t M,
+                          int64_t N, int64_t K, int64_t batch, int raster, int64_t pairs, void* stream) {
+    if (ta && tb) return launch_pair<NH, true, true>(ma, mb, C, M, N, K, batch, raster, pairs, stream);
+    if (ta) return launch_pair<NH, true, false>(ma, mb, C, M, N, K, batch, raster, pairs, stream);
+    if (tb) return launch_pair<NH, false, true>(ma, mb, C, M, N, K, batch, raster, pairs, stream);
+    return launch_pair<NH, false, false>(ma, mb, C, M, N, K, batch, raster, pairs, stream);
+}
 
-extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
-                                      int64_t batch, int32_t raster, void* stream) {
+lego_status gemm_impl(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int64_t batch,
+                      int32_t raster, int32_t a_major, int32_t b_major, void* stream) {
     if (M <= 0 || N <= 0 || K <= 0 || batch <= 0)
         return lego_fail(LEGO_E_SHAPE, "gemm shape must be positive");
-    if (N % 8 || K % 8)
-        return lego_fail(LEGO_E_SHAPE, "gemm needs N %% 8 == 0 and K %% 8 == 0 (16-byte rows; got N=%lld K=%lld)",
-                         (long long)N, (long long)K);
-    // exact tiles: single-CTA 128 x 256 when M % 256 != 0; anything ragged goes to the pair kernel
-    const bool ragged = M % BM || N % BN || K % BK;
+    if (a_major < 0 || a_major > 1 || b_major < 0 || b_major > 1)
+        return lego_fail(LEGO_E_ARG, "operand major must be 0 (K-major) or 1 (MN-major)");
+    const bool ta = a_major == 1, tb = b_major == 1;
+    // 16-byte rows for every TMA-read operand and for C
+    if (N % 8 || (!ta || !tb ? K % 8 : 0) || (ta && M % 8))
+        return lego_fail(LEGO_E_SHAPE,
+                         "gemm needs N %% 8 == 0, K %% 8 == 0 (K-major operands), M %% 8 == 0 (MN-major A); "
+                         "got M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
     if (M * batch > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
         return lego_fail(LEGO_E_SHAPE, "gemm dimensions too large");
     if (((uintptr_t)A | (uintptr_t)B | (uintptr_t)C) & 15)
@@ -693,18 +751,23 @@ extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int
         const char* e = getenv("LEGO_GEMM_PAIR");
         return !(e && e[0] == '0');
     }();
+    // exact tiles: single-CTA 128 x 256 when M % 256 != 0; ragged shapes and MN-major
+    // operands go to the pair kernel
+    const bool ragged = M % BM || N % BN || K % BK || ta || tb;
     if (ragged || (pair_ok && M % (2 * pair::BM) == 0 && N % pair::BN == 0)) {
         // CTA-pair kernel on cta_group::2: 256 x 512 tiles when N allows, else 256 x 256
         const bool wide = (ragged ? N > 256 : N % 512 == 0) && pair_wide();
         CUtensorMap ma, mb;
-        LEGO_TRY(make_map(&ma, A, M, K, batch, pair::BM));
-        LEGO_TRY(make_map(&mb, B, N, K, batch, 128));
+        if (ta) LEGO_TRY(make_map_mn(&ma, A, M, K, batch));
+        else LEGO_TRY(make_map(&ma, A, M, K, batch, pair::BM));
+        if (tb) LEGO_TRY(make_map_mn(&mb, B, N, K, batch));
+        else LEGO_TRY(make_map(&mb, B, N, K, batch, 128));
         const int64_t tn = wide ? 512 : 256;
         const int64_t tiles = ((M + 255) / 256) * ((N + tn - 1) / tn) * batch;
         const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
         const int g = raster > 1 ? raster / 2 : raster;   // G counts 128-row m-blocks; pair tiles are 256 rows
-        if (wide) return launch_pair<2>(ma, mb, C, M, N, K, batch, g, pairs, stream);
-        return launch_pair<1>(ma, mb, C, M, N, K, batch, g, pairs, stream);
+        if (wide) return dispatch_pair<2>(ta, tb, ma, mb, C, M, N, K, batch, g, pairs, stream);
+        return dispatch_pair<1>(ta, tb, ma, mb, C, M, N, K, batch, g, pairs, stream);
     }
     CUtensorMap ma, mb;
     LEGO_TRY(make_map(&ma, A, M, K, batch, BM));
@@ -720,4 +783,17 @@ extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int
     gemm_bf16_tcgen05<<<grid, NUM_THREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
         ma, mb, static_cast<__nv_bfloat16*>(C), (int)M, (int)N, (int)K, (int)batch, raster);
     return lego_cuda_check(cudaGetLastError(), "gemm launch");
+}
+
+}  // namespace
+
+extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
+                                      int64_t batch, int32_t raster, void* stream) {
+    return gemm_impl(A, B, C, M, N, K, batch, raster, 0, 0, stream);
+}
+
+extern "C" lego_status lego_gemm_bf16_ex(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
+                                         int64_t batch, int32_t raster, int32_t a_major, int32_t b_major,
+                                         void* stream) {
+    return gemm_impl(A, B, C, M, N, K, batch, raster, a_major, b_major, stream);
 }

@@ -456,21 +456,25 @@ def nw_score(sim, penalty: int, *, out=None, stream=None):
 GEMM_RASTER_GROUP = int(os.environ.get("LEGO_GEMM_GROUP", "16"))
 
 
-def gemm(a, b, *, out=None, raster: Optional[int] = None, stream=None):
+def gemm(a, b, *, out=None, raster: Optional[int] = None, a_col: bool = False, b_col: bool = False,
+         stream=None):
     """``C = A @ B.T`` for bf16 ``A (..., M, K)`` and ``B (..., N, K)`` on tcgen05.
 
-    ``raster`` = G selects the LEGO tile raster
-    ``GroupBy([MB/G, NB, G]).OrderBy(Row(MB/G, NB, G))`` (0 = row-major)."""
+    ``a_col`` / ``b_col``: the operand is passed MN-major instead, ``a`` as
+    ``(..., K, M)`` (A = a^T) and ``b`` as ``(..., K, N)`` (B = b^T) -- the
+    Row/Col operand data layouts of the paper's matmul variants, consumed
+    directly as MN-major UMMA operands.  ``raster`` = G selects the LEGO tile
+    raster ``GroupBy([MB/G, NB, G]).OrderBy(Row(MB/G, NB, G))`` (0 = row-major)."""
     if raster is None:
         raster = GEMM_RASTER_GROUP
     torch = _torch()
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or not a.is_cuda:
         raise ShapeMismatch("gemm takes CUDA bfloat16 tensors")
     a, b = a.contiguous(), b.contiguous()
-    M, K = a.shape[-2], a.shape[-1]
-    N = b.shape[-2]
-    if b.shape[-1] != K:
-        raise ShapeMismatch(f"inner dims differ: {K} vs {b.shape[-1]}")
+    K, M = (a.shape[-2], a.shape[-1]) if a_col else (a.shape[-1], a.shape[-2])
+    Kb, N = (b.shape[-2], b.shape[-1]) if b_col else (b.shape[-1], b.shape[-2])
+    if Kb != K:
+        raise ShapeMismatch(f"inner dims differ: {K} vs {Kb}")
     batch = 1
     for d in a.shape[:-2]:
         batch *= d
@@ -480,11 +484,25 @@ def gemm(a, b, *, out=None, raster: Optional[int] = None, stream=None):
         return out
     if K == 0:
         return out.zero_()
-    runtime.check(runtime.lib().lego_gemm_bf16(a.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K,
-                                               batch, raster, runtime.stream_handle(stream)),
-                  "lego_gemm_bf16")
+    runtime.check(runtime.lib().lego_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K,
+                                                  batch, raster, int(a_col), int(b_col),
+                                                  runtime.stream_handle(stream)),
+                  "lego_gemm_bf16_ex")
     LAUNCHES[0] += 1
     return out
+
+
+def matmul(a, b, *, a_layout: str = "row", b_layout: str = "row", out=None, **kw):
+    """``C = A @ B`` with ``A`` (M x K) and ``B`` (K x N) given in the Row or Col
+    data layout of the paper's four matmul variants: a
+    Row operand is stored row-major, a Col operand column-major (i.e. the
+    tensor passed holds its transpose, ``A^T`` as (..., K, M) / ``B^T`` as
+    (..., N, K)).  Every variant runs as one tcgen05 GEMM; nothing is
+    transposed in memory."""
+    if a_layout not in ("row", "col") or b_layout not in ("row", "col"):
+        raise ShapeMismatch("a_layout / b_layout must be 'row' or 'col'")
+    # gemm computes A @ B'^T with B' = B^T given K-major (N x K) or MN-major (K x N)
+    return gemm(a, b, out=out, a_col=a_layout == "col", b_col=b_layout == "row", **kw)
 
 
 def _ensure_var(v) -> Var:

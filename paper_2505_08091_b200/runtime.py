@@ -77,6 +77,7 @@ SIGS = {
     "lego_softmax_f32": ([VP, VP, I64, I64, VP], I32),
     "lego_nw_i32": ([VP, VP, I64, I32, I64, VP], I32),
     "lego_gemm_bf16": ([VP, VP, VP, I64, I64, I64, I64, I32, VP], I32),
+    "lego_gemm_bf16_ex": ([VP, VP, VP, I64, I64, I64, I64, I32, I32, I32, VP], I32),
 }
 
 

@@ -96,3 +96,22 @@ def test_empty_inputs():
     c = K.gemm(torch.empty(0, 128, 64, device="cuda", dtype=torch.bfloat16),
                torch.empty(0, 256, 64, device="cuda", dtype=torch.bfloat16))
     assert c.shape == (0, 128, 256)
+
+
+@pytest.mark.parametrize("a_layout", ["row", "col"])
+@pytest.mark.parametrize("b_layout", ["row", "col"])
+@pytest.mark.parametrize("M,N,Kd,batch", [(256, 512, 128, 1), (512, 768, 320, 2), (136, 264, 72, 1),
+                                          (2048, 2048, 2048, 1)])
+def test_matmul_four_data_layouts(a_layout, b_layout, M, N, Kd, batch):
+    """The paper's four matmul variants (Row/Col data layout of A and B,
+    PAPER.md:1226-1227): MN-major operands go to tcgen05 directly."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + Kd)
+    A = torch.randn(batch, M, Kd, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(batch, Kd, N, device="cuda", generator=g).to(torch.bfloat16)
+    a = A if a_layout == "row" else A.transpose(-1, -2).contiguous()      # Col: stored column-major
+    b = B if b_layout == "row" else B.transpose(-1, -2).contiguous()
+    c = K.matmul(a, b, a_layout=a_layout, b_layout=b_layout)
+    ref = torch.matmul(A.double(), B.double())
+    denom = torch.clamp(ref.abs(), min=1e-2 * ref.abs().max().item())
+    rel = ((c.double() - ref).abs() / denom).max().item()
+    assert rel <= 1e-2, (a_layout, b_layout, M, N, Kd, rel)
