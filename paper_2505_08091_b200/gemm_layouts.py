@@ -1,0 +1,60 @@
+"""The GEMM's data, thread and shared-memory layouts written as LEGO layouts.
+
+* ``raster_layout(mb, nb, g)`` -- the CTA tile raster walked by
+  ``csrc/gemm_tcgen05.cu`` (``Raster::coords`` evaluates its inverse).
+* ``sw128_perm()`` -- the 128-byte shared-memory swizzle that TMA
+  (``CU_TENSOR_MAP_SWIZZLE_128B``) writes and the UMMA descriptors
+  (layout type 2) read: inside a 1024-byte atom of 8 rows x 8 16-byte chunks,
+  chunk ``c`` of row ``r`` sits at chunk ``c XOR r``.  A user-defined LEGO
+  bijection (``GenP``) whose symbolic builder spells XOR with ``//`` and ``%``
+  on the three chunk bits, so the CUDA code generator can emit it.
+* ``kmajor_smem_layout(rows, k)`` -- a K-major bf16 operand tile
+  (``rows`` x ``k``, k = 64 per 128-byte row) in that swizzle:
+  ``GroupBy([rows/8, 8, 8, 8]).OrderBy(Row(rows/8), GenP([8,8], sw128), Row(8))``
+  over (row_hi, row_lo, chunk, element).
+"""
+
+from __future__ import annotations
+
+from .layout import GenP, GroupBy, OrderBy, PermFn, RegP
+from .dsl import parse_layout
+
+
+def _xor3(a, b):
+    """a XOR b for 0 <= a, b < 8, with only +, //, % (works on ints and Exprs)."""
+    return sum((((a // (1 << k)) % 2 + (b // (1 << k)) % 2) % 2) * (1 << k) for k in range(3))
+
+
+def sw128_perm() -> GenP:
+    """(row r, chunk c) of an 8 x 8 atom -> r*8 + (c XOR r)."""
+    def fwd(idx):
+        r, c = idx
+        return r * 8 + (c ^ r)
+
+    def fwd_sym(idx):
+        r, c = idx
+        return r * 8 + _xor3(c, r)
+
+    def inv(flat):
+        r, x = divmod(flat, 8)
+        return r, x ^ r
+
+    def inv_sym(flat):
+        r = flat // 8
+        return r, _xor3(flat % 8, r)
+
+    return GenP((8, 8), PermFn(fwd, fwd_sym), PermFn(inv, inv_sym), name="sw128")
+
+
+def kmajor_smem_layout(rows: int, k: int = 64) -> GroupBy:
+    """Element offsets of a K-major bf16 tile (rows x k, 128-byte rows) in the
+    SWIZZLE_128B layout; k must be 64 (one swizzle row of bf16)."""
+    if rows % 8 or k != 64:
+        raise ValueError("rows % 8 == 0 and k == 64 (bf16 128-byte swizzle rows)")
+    return GroupBy([rows // 8, 8, 8, 8], orders=(OrderBy(RegP([rows // 8], [1]), sw128_perm(),
+                                                         RegP([8], [1])),))
+
+
+def raster_layout(mb: int, nb: int, g: int) -> GroupBy:
+    """Tile raster: tile t -> (group, n-block, m within group), m fastest."""
+    return parse_layout(f"GroupBy([{mb // g},{nb},{g}]).OrderBy(Row({mb // g},{nb},{g}))")
