@@ -403,6 +403,14 @@ def other_kernels(args, pk, world):
               lambda: K.remap(x4, None, g4, out=y4), "remap_antidiag_i32",
               {"plan": repr(K.remap_plan(None, g4, 4))})
     del x4, y4
+    # cfg4 index maps: every apply / inv of the antidiag layout (inv needs an exact isqrt)
+    m4 = torch.empty(16384 * 16384, device="cuda", dtype=torch.int32)
+    for which, fn in (("apply", K.apply_map), ("inv", K.inv_map)):
+        ms = time_steps(lambda: fn(g4, out=m4), steps, warm, world) / steps
+        res[f"cfg4_antidiag_{which}_map_i32"] = {
+            "Gidx/s": round(m4.numel() / (ms * 1e-3) / 1e9, 1), "GB/s": round(m4.numel() * 4 / (ms * 1e-3) / 1e9, 1),
+            "frac": round(m4.numel() * 4 / (ms * 1e-3) / 1e9 / pk["hbm"], 4), "us": round(ms * 1e3, 1)}
+    del m4
     # cfg4b: NW wavefront 16384^2 int32
     try:
         sim = torch.randint(-10, 11, (16384, 16384), device="cuda", dtype=torch.int32)

@@ -73,12 +73,17 @@ class DeviceFunction:
         return f"DeviceFunction({self.name}, ops={self.n_ops})"
 
 
-def generate(name: str, inputs: Sequence[Var], outputs: Mapping[str, Expr]) -> DeviceFunction:
+def generate(name: str, inputs: Sequence[Var], outputs: Mapping[str, Expr],
+             bounds: Mapping[str, Tuple[int, int]] = None) -> DeviceFunction:
     """``static __device__ __forceinline__ void name(long long in..., T& out...)``.
 
     Inputs arrive as ``long long`` (the kernel's flat indices); each output
-    is written through a reference of its own width.
+    is written through a reference of its own width.  ``bounds`` states true
+    value ranges of outputs that interval analysis cannot prove (e.g. a
+    layout inverse lands in [0, size) although its terms cancel); an output
+    whose bound fits 32 bits lets the terms feeding it compute mod 2^32.
     """
+    bounds = dict(bounds or {})
     iv = Intervals()
     for v in inputs:
         if v.range is None:
@@ -90,6 +95,55 @@ def generate(name: str, inputs: Sequence[Var], outputs: Mapping[str, Expr]) -> D
             if n not in seen:
                 seen.add(n)
                 order.append(n)
+    # Modular narrowing: a node whose every use is an operand of +, -, * or a
+    # Select arm, leading only to values that fit 32 bits, can be computed
+    # mod 2^32 (ring homomorphism) in `unsigned` even when its own range does
+    # not fit -- e.g. the anti-diagonal inverse's i*16383 terms that cancel.
+    uses: Dict[Expr, List[Tuple[Expr, str]]] = {}
+
+    def _cond_nodes(c, acc):
+        if type(c) is Cmp:
+            acc.extend([c.lhs, c.rhs])
+        elif type(c) is And:
+            _cond_nodes(c.lhs, acc)
+            _cond_nodes(c.rhs, acc)
+
+    for n in order:
+        t = type(n)
+        if t in (Add, Sub, Mul):
+            for ch in (n.lhs, n.rhs):
+                uses.setdefault(ch, []).append((n, "ring"))
+        elif t is Select:
+            for ch in (n.then, n.orelse):
+                uses.setdefault(ch, []).append((n, "arm"))
+            acc: List[Expr] = []
+            _cond_nodes(n.cond, acc)
+            for ch in acc:
+                uses.setdefault(ch, []).append((n, "other"))
+        else:
+            for ch in children(n):
+                uses.setdefault(ch, []).append((n, "other"))
+    out_fits = {}
+    for oname, e in outputs.items():
+        fits = _fits32(iv.of(e)) or (oname in bounds and _fits32(bounds[oname]))
+        out_fits[oname] = fits
+        uses.setdefault(e, []).append((e, "out32" if fits else "other"))
+    modsafe: Dict[Expr, bool] = {}
+
+    def _modsafe(n) -> bool:
+        if n in modsafe:
+            return modsafe[n]
+        modsafe[n] = False                      # cycle guard (DAGs have none)
+        ok = bool(uses.get(n))
+        for parent, role in uses.get(n, []):
+            if role == "out32":
+                continue
+            if role not in ("ring", "arm") or not (_fits32(iv.of(parent)) or _modsafe(parent)):
+                ok = False
+                break
+        modsafe[n] = ok
+        return ok
+
     # conditions are not Exprs; generate their sub-expressions via Select
     names: Dict[Expr, str] = {}
     types: Dict[Expr, str] = {}
@@ -134,7 +188,8 @@ def generate(name: str, inputs: Sequence[Var], outputs: Mapping[str, Expr]) -> D
             emit(ch)
         t = type(node)
         r = iv.of(node)
-        res_t = "int" if _fits32(r) else "long long"
+        res_t = "int" if _fits32(r) else ("unsigned" if t in (Add, Sub, Mul, Select) and _modsafe(node)
+                                          else "long long")
         if t is IntConst:
             v = node.value
             if _fits32((v, v)):
@@ -151,6 +206,13 @@ def generate(name: str, inputs: Sequence[Var], outputs: Mapping[str, Expr]) -> D
         n_ops += 1
         if t in (Add, Sub, Mul):
             op = {Add: "+", Sub: "-", Mul: "*"}[t]
+            if res_t == "unsigned" or "int" != types[node.lhs] or "int" != types[node.rhs] and res_t == "int":
+                if res_t == "long long":
+                    tmp(res_t, f"{cast(node.lhs, res_t)} {op} {cast(node.rhs, res_t)}", node)
+                else:   # wrapping 32-bit arithmetic (exact mod 2^32)
+                    text = f"{cast(node.lhs, 'unsigned')} {op} {cast(node.rhs, 'unsigned')}"
+                    tmp(res_t, text if res_t == "unsigned" else f"(int)({text})", node)
+                return
             tmp(res_t, f"{cast(node.lhs, res_t)} {op} {cast(node.rhs, res_t)}", node)
             return
         if t is FloorDiv or t is Mod:
@@ -204,7 +266,10 @@ def generate(name: str, inputs: Sequence[Var], outputs: Mapping[str, Expr]) -> D
         # (int when it fits) is what the arithmetic above used
         out_types.append("long long")
         sig_out.append(f"long long& {oname}")
-        body_out.append(f"  {oname} = {cast(e, 'long long')};")
+        if types.get(e) == "unsigned":          # wrapped value whose true range fits int
+            body_out.append(f"  {oname} = (long long)(int){names[e]};")
+        else:
+            body_out.append(f"  {oname} = {cast(e, 'long long')};")
     sig = ", ".join([s for s in (sig_in, ", ".join(sig_out)) if s])
     src = (f"static __device__ __forceinline__ void {name}({sig}) {{\n"
            + "\n".join(lines + body_out) + "\n}\n")

@@ -30,11 +30,13 @@ static __device__ __forceinline__ auto lego_fmod(A a, B b) -> decltype(a + b) {
 
 // exact floor(sqrt(x)); negative arguments clamp to 0 (only reachable in the
 // untaken arm of a select, which the generated code evaluates eagerly)
+// 32-bit: x < 2^31, so float(x) and the rounded sqrt are within 0.01 of
+// sqrt(x) and one branch-free correction step each way is exact
 static __device__ __forceinline__ int lego_isqrt32(int x) {
     if (x <= 0) return 0;
-    int r = (int)sqrtf((float)x);
-    while ((long long)r * r > x) --r;
-    while ((long long)(r + 1) * (r + 1) <= x) ++r;
+    int r = (int)__fsqrt_rn((float)x);
+    r -= ((unsigned)r * (unsigned)r > (unsigned)x) ? 1 : 0;
+    r += ((unsigned)(r + 1) * (unsigned)(r + 1) <= (unsigned)x) ? 1 : 0;
     return r;
 }
 static __device__ __forceinline__ long long lego_isqrt64(long long x) {

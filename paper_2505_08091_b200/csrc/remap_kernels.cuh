@@ -74,16 +74,37 @@ template <> struct lego_elem<8> { typedef unsigned long long t; };
 #if LEGO_KIND == 0
 // index maps: one thread per output element, int32 or int64 outputs.
 template <typename T>
+static __device__ __forceinline__ T lego_map_one(long long x, int which) {
+    long long r;
+    if (which == 0) gen::apply_fn(x, r);
+    else            gen::inv_fn(x, r);
+    return (T)r;
+}
+// 4 consecutive indices per thread and one 16-byte (int32) / two 16-byte
+// (int64) stores when the output is 16-byte aligned; scalar tail
+template <typename T>
 static __device__ __forceinline__ void lego_map_body(T* out, long long first, long long count,
                                                      int which) {
-    long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (; k < count; k += stride) {
-        long long v;
-        if (which == 0) { long long r; gen::apply_fn(first + k, r); v = r; }
-        else            { long long r; gen::inv_fn(first + k, r); v = r; }
-        out[k] = (T)v;
+    long long done = 0;
+    if ((reinterpret_cast<unsigned long long>(out) & 15) == 0) {
+        const long long nq = count >> 2;
+        for (long long q = tid; q < nq; q += stride) {
+            const long long x = first + 4 * q;
+            T v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = lego_map_one<T>(x + u, which);
+            if (sizeof(T) == 4) {
+                *reinterpret_cast<int4*>(out + 4 * q) = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+            } else {
+                *reinterpret_cast<longlong2*>(out + 4 * q) = make_longlong2((long long)v[0], (long long)v[1]);
+                *reinterpret_cast<longlong2*>(out + 4 * q + 2) = make_longlong2((long long)v[2], (long long)v[3]);
+            }
+        }
+        done = nq << 2;
     }
+    for (long long k = done + tid; k < count; k += stride) out[k] = lego_map_one<T>(first + k, which);
 }
 LEGO_GLOBAL void __launch_bounds__(256) lego_apply_map_i32(int* out, long long first, long long count) {
     lego_map_body<int>(out, first, count, 0);

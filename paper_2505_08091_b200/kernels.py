@@ -85,12 +85,14 @@ def index_map_source(layout) -> Tuple[str, runtime.ProgramInfo]:
     injective = getattr(lower._group(layout), "injective", False)
     body = codegen.constant("N", lower.logical_size(layout))
     body += codegen.constant("M", lower.physical_size(layout))
-    body += codegen.generate("apply_fn", [x], {"out": app}).source
+    body += codegen.generate("apply_fn", [x], {"out": app},
+                             bounds={"out": (-1, lower.physical_size(layout) - 1)}).source
     if injective:
         body += "static __device__ __forceinline__ void inv_fn(const long long f, long long& out) { out = -1; }\n"
     else:
         f, inv = lower.inv_map_expr(layout)
-        body += codegen.generate("inv_fn", [f], {"out": inv}).source
+        body += codegen.generate("inv_fn", [f], {"out": inv},
+                                 bounds={"out": (0, lower.logical_size(layout) - 1)}).source
     info = runtime.ProgramInfo(kind=runtime.KIND_INDEX_MAP, elem_bytes=0,
                                n=lower.logical_size(layout), units=lower.physical_size(layout),
                                unit_threads=1, block=256, smem_bytes=0)
@@ -161,7 +163,7 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
         # 16-byte source vectors would straddle batch entries
         return _scalar_gather_plan(f, g, n_dst, n_src, elem_bytes, masked)
     body = codegen.constant("N", n_dst)
-    body += codegen.generate("src_of", [f], {"s": g}).source
+    body += codegen.generate("src_of", [f], {"s": g}, bounds={"s": (-1, n_src - 1)}).source
     unroll = 4
     block = 256
     nvec = n_dst // vec
@@ -178,7 +180,8 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
 def _scalar_gather_plan(f, g, n_dst, n_src, elem_bytes, masked) -> RemapPlan:
     """Ragged sizes (n_dst not a whole number of 16-byte vectors, or source
     batch strides that are not 16-byte multiples): one element per thread."""
-    body = codegen.constant("N", n_dst) + codegen.generate("src_of", [f], {"s": g}).source
+    body = codegen.constant("N", n_dst) + codegen.generate("src_of", [f], {"s": g},
+                                                            bounds={"s": (-1, n_src - 1)}).source
     units = max(1, min((n_dst + 255) // 256, 148 * 16))
     info = runtime.ProgramInfo(kind=runtime.KIND_GATHER, elem_bytes=elem_bytes, n=n_dst,
                                units=units, unit_threads=1, block=256, smem_bytes=0,
@@ -240,7 +243,7 @@ def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
     pos = lower.simplify(lower.as_expr(lower.apply_flat(side, x)))
     kblocks = (n + br + bk - 2) // bk + 1
     body = codegen.constant("NN", n) + codegen.constant("KBLOCKS", kblocks)
-    body += codegen.generate("pos_of", [x], {"p": pos}).source
+    body += codegen.generate("pos_of", [x], {"p": pos}, bounds={"p": (0, n * n - 1)}).source
     order = BAND_ORDER if BAND_ORDER >= 0 else (1 if direction == 0 else 0)
     if order == 0:
         units = (n // br) * kblocks

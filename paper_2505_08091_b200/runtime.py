@@ -118,11 +118,16 @@ def device_info(device: int = 0):
     return {"sm_count": sm.value, "l2_bytes": l2.value, "cc": (ma.value, mi.value)}
 
 
+def cubin_path(source: str) -> str:
+    """Cache file of a program text (SHA-256 of arch + source)."""
+    key = hashlib.sha256((ARCH + "\0" + source).encode()).hexdigest()[:32]
+    return os.path.join(CACHE_DIR, key + ".cubin")
+
+
 def compile_cubin(source: str) -> bytes:
     """NVRTC-compile a generated program for sm_100a, cached on disk by the
     SHA-256 of its text (the cache travels with the repo snapshot)."""
-    key = hashlib.sha256((ARCH + "\0" + source).encode()).hexdigest()[:32]
-    path = os.path.join(CACHE_DIR, key + ".cubin")
+    path = cubin_path(source)
     if os.path.exists(path):
         with open(path, "rb") as fh:
             return fh.read()
