@@ -30,11 +30,15 @@ static __device__ __forceinline__ auto lego_fmod(A a, B b) -> decltype(a + b) {
 
 // exact floor(sqrt(x)); negative arguments clamp to 0 (only reachable in the
 // untaken arm of a select, which the generated code evaluates eagerly)
-// 32-bit: x < 2^31, so float(x) and the rounded sqrt are within 0.01 of
-// sqrt(x) and one branch-free correction step each way is exact
+// 32-bit: x < 2^31, so float(x) (rel. error 2^-24) and the approximate
+// MUFU square root (rel. error ~2^-22) land within 0.02 of sqrt(x) <= 46341;
+// the truncated root is off by at most one and one branch-free correction
+// step each way is exact
 static __device__ __forceinline__ int lego_isqrt32(int x) {
     if (x <= 0) return 0;
-    int r = (int)__fsqrt_rn((float)x);
+    float fr;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(fr) : "f"((float)x));
+    int r = (int)fr;
     r -= ((unsigned)r * (unsigned)r > (unsigned)x) ? 1 : 0;
     r += ((unsigned)(r + 1) * (unsigned)(r + 1) <= (unsigned)x) ? 1 : 0;
     return r;
