@@ -366,6 +366,11 @@ def run(args):
         dist.destroy_process_group()
 
 
+def lower_size(layout):
+    from paper_2505_08091_b200 import lower
+    return lower.physical_size(layout)
+
+
 def other_kernels(args, pk, world):
     """The remaining BASELINE configs, timed the same way (W warm-up, K steps)."""
     import torch
@@ -411,6 +416,27 @@ def other_kernels(args, pk, world):
             "Gidx/s": round(m4.numel() / (ms * 1e-3) / 1e9, 1), "GB/s": round(m4.numel() * 4 / (ms * 1e-3) / 1e9, 1),
             "frac": round(m4.numel() * 4 / (ms * 1e-3) / 1e9 / pk["hbm"], 4), "us": round(ms * 1e3, 1)}
     del m4
+    # SURVEY section 8(f) rows at scale (parity-tested in tests/): f1 multi-stage chain with an
+    # in-tile GenP (Eq. (2) shape), f2 ExpandBy partial tiles, f4 injective scatter
+    def frow(name, layout, n_elems, direction, dtype=torch.int32, scatter=False):
+        x = torch.arange(n_elems, device="cuda", dtype=torch.int64).to(dtype)
+        src_l, dst_l = (None, layout) if direction == "to" else (layout, None)
+        out = K.remap(x, src_l, dst_l)
+        fn = lambda: K.remap(x, src_l, dst_l, out=out)  # noqa: E731
+        plan = K.remap_plan(src_l, dst_l, x.element_size())
+        # bytes: each source element read once, each written destination element once
+        nbytes = (2 * x.numel() if scatter else x.numel() + out.numel()) * x.element_size()
+        hbm_entry(name, nbytes, fn, None, {"plan": repr(plan)})
+        del x, out
+    f1 = L.parse_layout("GroupBy([8192,8192]).OrderBy(RegP([128,64,128,64],[1,3,2,4]))"
+                        ".OrderBy(RegP([128,128],[2,1]), GenP([64,64], antidiag))")
+    frow("f1_chain_tile_antidiag_8192_i32", f1, 8192 * 8192, "to")
+    f2 = L.parse_layout("ExpandBy([8000,8000],[8192,8192],"
+                        "GroupBy([8192,8192]).OrderBy(RegP([128,64,128,64],[1,3,2,4])))")
+    frow("f2_expand_partial_tiles_i32", f2, lower_size(f2), "from")
+    even = L.GenP((1 << 26,), L.PermFn(lambda idx: idx[0] * 2, lambda idx: idx[0] * 2), None, name="even")
+    f4 = L.GroupBy([1 << 26], orders=(L.OrderBy(even),), injective=True)
+    frow("f4_injective_even_scatter_i32", f4, 1 << 26, "to", scatter=True)
     # cfg4b: NW wavefront 16384^2 int32
     try:
         sim = torch.randint(-10, 11, (16384, 16384), device="cuda", dtype=torch.int32)
