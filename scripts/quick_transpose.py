@@ -13,7 +13,7 @@ g = L.parse_layout("GroupBy([16384,16384]).OrderBy(Col(16384,16384))")
 for dt in (torch.bfloat16, torch.float32):
     src = torch.randint(0, 100, (16384 * 16384,), device="cuda").to(dt)
     out = torch.empty_like(src)
-    for var in ("reg", "regT", "smem"):
+    for var in (sys.argv[1:] or ["reg", "regT", "smem"]):
         for order in ("x", "y", "block"):
             K.TRANSPOSE_VARIANT = var
             K.TILE_ORDER = order
