@@ -54,7 +54,8 @@ typedef enum {
     LEGO_PROG_GATHER = 1,      /* remap: dst[f] = src[g(f)], per-element g             */
     LEGO_PROG_TRANSPOSE = 2,   /* remap: digit-permutation, register-tiled transpose   */
     LEGO_PROG_BAND = 3,        /* remap: anti-diagonal band tiles through shared memory */
-    LEGO_PROG_SCATTER = 4      /* remap into an injective layout: dst[apply(x)] = src[x] */
+    LEGO_PROG_SCATTER = 4,     /* remap into an injective layout: dst[apply(x)] = src[x] */
+    LEGO_PROG_STAGED = 5       /* remap: per-block source box staged through smem      */
 } lego_program_kind;
 
 /* Program geometry.  Index-map programs: n = logical size, units = physical

@@ -17,6 +17,9 @@
 //                             16-byte loads along src rows and 16-byte stores
 //                             along dst rows, transposed in registers
 //   LEGO_KIND 3  band:        anti-diagonal band tiles staged through smem
+//   LEGO_KIND 4  scatter:     dst[apply(x)] = src[x] into an injective layout
+//   LEGO_KIND 5  staged:      each destination block reads one source box,
+//                             staged through smem (staging.py's proof)
 #pragma once
 
 #define LEGO_GLOBAL extern "C" __global__
@@ -573,4 +576,166 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
     }
 }
 #endif  // LEGO_SCALAR
+#endif
+
+// ---------------------------------------------------------------------------
+#if LEGO_KIND == 5
+// box-staged gather (paper_2505_08091_b200/staging.py): the planner proved
+// g(q*B + r) == base(q) + row(r)*SX + col(r), so destination block q (B
+// consecutive elements) reads only the source box of R rows x C elements at
+// stride SX starting at base(q), and reads every cell of it (so every cell is
+// a valid source element: no bounds checks).  A CTA owns one block: coalesced (16-byte
+// where aligned) loads of the box into shared memory (row pitch PITCH), then
+// coalesced stores of the block, each element read from its box cell
+// gen::TAB[r] = row(r)*PITCH + col(r) (a per-layout table, L1-resident).
+//   LEGO_LVEC   box rows are whole 16-byte vectors at 16-byte stride (C*E and
+//               SX*E multiples of 16); the start address is checked per CTA
+//   LEGO_SVEC16 PITCH*E is a multiple of 16: box vectors stored whole
+//   LEGO_VSTORE each thread stores V consecutive destination elements (one
+//               16-byte store), else one element per lane
+typedef lego_elem<LEGO_ELEM>::t lego_e;
+#define LEGO_V (16 / LEGO_ELEM)
+#define LEGO_BT 256                                    // threads per CTA
+struct alignas(sizeof(gen::tab_t) * LEGO_V) lego_tabv { gen::tab_t t[LEGO_V]; };
+
+#if LEGO_SCATTER
+// mirrored form: source block q (B consecutive elements) lands in the
+// destination box at base(q) (R rows x C at stride SX): 16-byte loads of the
+// block, scattered into the box cells gen::TAB[r], then box rows stored
+// coalesced (16-byte where the row start is aligned).
+LEGO_GLOBAL void __launch_bounds__(LEGO_BT) lego_remap(const unsigned char* __restrict__ src,
+                                                       unsigned char* __restrict__ dst,
+                                                       long long src_stride, long long dst_stride) {
+    extern __shared__ __align__(16) unsigned char lego_smem[];
+    lego_e* box = reinterpret_cast<lego_e*>(lego_smem);
+    const long long q = blockIdx.x;
+    const lego_e* s = reinterpret_cast<const lego_e*>(src) + (long long)blockIdx.y * src_stride + q * gen::B;
+    lego_e* d = reinterpret_cast<lego_e*>(dst) + (long long)blockIdx.y * dst_stride;
+    long long b0;
+    gen::base_of(q, b0);
+    const int tid = threadIdx.x;
+    if ((reinterpret_cast<unsigned long long>(s) & 15) == 0) {
+        constexpr int NV = gen::B / LEGO_V;
+        constexpr int IT = (NV + LEGO_BT - 1) / LEGO_BT;
+        lego_v16 v[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int k = it * LEGO_BT + tid;
+            if (k < NV) v[it] = lego_ld16(reinterpret_cast<const unsigned char*>(s + (long long)k * LEGO_V));
+        }
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int k = it * LEGO_BT + tid;
+            if (k >= NV) break;
+            const lego_tabv tv = reinterpret_cast<const lego_tabv*>(gen::TAB)[k];
+            union { lego_v16 v; lego_e e[LEGO_V]; } u;
+            u.v = v[it];
+#pragma unroll
+            for (int e = 0; e < LEGO_V; ++e) box[tv.t[e]] = u.e[e];
+        }
+    } else {
+#pragma unroll 8
+        for (int r = tid; r < gen::B; r += LEGO_BT) box[gen::TAB[r]] = __ldg(s + r);
+    }
+    __syncthreads();
+    lego_e* db = d + b0;
+#if LEGO_LVEC
+    if ((reinterpret_cast<unsigned long long>(db) & 15) == 0) {
+        constexpr int VPR = gen::C / LEGO_V;
+        constexpr int NV = gen::R * VPR;
+#pragma unroll 4
+        for (int k = tid; k < NV; k += LEGO_BT) {
+            const int row = k / VPR, cv = k - row * VPR;
+#if LEGO_SVEC16
+            const lego_v16 v = *reinterpret_cast<const lego_v16*>(box + row * gen::PITCH + cv * LEGO_V);
+#else
+            union { lego_v16 v; lego_e e[LEGO_V]; } u;
+#pragma unroll
+            for (int e = 0; e < LEGO_V; ++e) u.e[e] = box[row * gen::PITCH + cv * LEGO_V + e];
+            const lego_v16 v = u.v;
+#endif
+            lego_st16(reinterpret_cast<unsigned char*>(db + (long long)row * gen::SX + cv * LEGO_V), v);
+        }
+    } else
+#endif
+    {
+        constexpr int NC = gen::R * gen::C;
+#pragma unroll 8
+        for (int k = tid; k < NC; k += LEGO_BT) {
+            const int row = k / gen::C, col = k - row * gen::C;
+            db[(long long)row * gen::SX + col] = box[row * gen::PITCH + col];
+        }
+    }
+}
+#else
+LEGO_GLOBAL void __launch_bounds__(LEGO_BT) lego_remap(const unsigned char* __restrict__ src,
+                                                       unsigned char* __restrict__ dst,
+                                                       long long src_stride, long long dst_stride) {
+    extern __shared__ __align__(16) unsigned char lego_smem[];
+    lego_e* box = reinterpret_cast<lego_e*>(lego_smem);
+    const long long q = blockIdx.x;
+    const lego_e* s = reinterpret_cast<const lego_e*>(src) + (long long)blockIdx.y * src_stride;
+    lego_e* d = reinterpret_cast<lego_e*>(dst) + (long long)blockIdx.y * dst_stride + q * gen::B;
+    long long b0;
+    gen::base_of(q, b0);
+    const int tid = threadIdx.x;
+#if LEGO_LVEC
+    const lego_e* sb = s + b0;
+    if ((reinterpret_cast<unsigned long long>(sb) & 15) == 0) {
+        constexpr int VPR = gen::C / LEGO_V;                 // vectors per box row
+        constexpr int NV = gen::R * VPR;
+        constexpr int IT = (NV + LEGO_BT - 1) / LEGO_BT;
+        lego_v16 v[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int k = it * LEGO_BT + tid;
+            const int row = k / VPR, cv = k - row * VPR;
+            if (k < NV)
+                v[it] = lego_ld16(reinterpret_cast<const unsigned char*>(sb + (long long)row * gen::SX + cv * LEGO_V));
+        }
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int k = it * LEGO_BT + tid;
+            const int row = k / VPR, cv = k - row * VPR;
+            if (k >= NV) break;
+#if LEGO_SVEC16
+            *reinterpret_cast<lego_v16*>(box + row * gen::PITCH + cv * LEGO_V) = v[it];
+#else
+            union { lego_v16 v; lego_e e[LEGO_V]; } u;
+            u.v = v[it];
+#pragma unroll
+            for (int e = 0; e < LEGO_V; ++e) box[row * gen::PITCH + cv * LEGO_V + e] = u.e[e];
+#endif
+        }
+    } else
+#endif
+    {
+        constexpr int NC = gen::R * gen::C;
+        constexpr int IT = (NC + LEGO_BT - 1) / LEGO_BT;
+#pragma unroll 8
+        for (int it = 0; it < IT; ++it) {
+            const int k = it * LEGO_BT + tid;
+            if (k >= NC) break;
+            const int row = k / gen::C, col = k - row * gen::C;
+            const long long si = b0 + (long long)row * gen::SX + col;
+            box[row * gen::PITCH + col] = __ldg(s + si);
+        }
+    }
+    __syncthreads();
+#if LEGO_VSTORE
+    constexpr int NO = gen::B / LEGO_V;
+#pragma unroll 4
+    for (int k = tid; k < NO; k += LEGO_BT) {
+        const lego_tabv tv = reinterpret_cast<const lego_tabv*>(gen::TAB)[k];
+        union { lego_v16 v; lego_e e[LEGO_V]; } u;
+#pragma unroll
+        for (int e = 0; e < LEGO_V; ++e) u.e[e] = box[tv.t[e]];
+        lego_st16(reinterpret_cast<unsigned char*>(d + (long long)k * LEGO_V), u.v);
+    }
+#else
+#pragma unroll 8
+    for (int r = tid; r < gen::B; r += LEGO_BT) d[r] = box[gen::TAB[r]];
+#endif
+}
+#endif  // LEGO_SCATTER
 #endif

@@ -30,7 +30,7 @@ import os
 import threading
 from typing import Dict, Optional, Tuple
 
-from . import codegen, lower, runtime
+from . import codegen, lower, runtime, staging
 from .errors import BijectivityViolation, ShapeMismatch, UnsupportedNode
 from .expr import Var
 
@@ -108,7 +108,7 @@ class RemapPlan:
         self.source, self.info, self.detail = source, info, detail
 
     def __repr__(self):
-        names = {1: "gather", 2: "transpose", 3: "band", 4: "scatter"}
+        names = {1: "gather", 2: "transpose", 3: "band", 4: "scatter", 5: "staged"}
         return (f"RemapPlan({names[self.kind]}, n={self.n_dst}, elem={self.elem_bytes}B, "
                 f"{self.detail})")
 
@@ -159,6 +159,17 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
                              info, f"tile {tp.tx}x{tp.ty} {variant}, SX={tp.sx}, DY={tp.dy}")
     width = 1 if masked else lower.contiguous_width(g, f, n_dst, widths=(vec,))
     contig = width >= vec
+    if not contig and BOX_STAGING:
+        bp = staging.box_plan(g, f, n_dst, n_src, elem_bytes) if not masked else None
+        if bp is not None:
+            return _staged_plan(bp, n_dst, n_src, elem_bytes)
+        if _mirrorable(src_layout, dst_layout):
+            # the mirrored form: h = g^-1 maps source positions to destination
+            # positions; source blocks land in destination boxes
+            fh, h, _, _ = lower.gather_expr(dst_layout, src_layout)
+            bp = staging.box_plan(h, fh, n_src, n_dst, elem_bytes)
+            if bp is not None:
+                return _staged_plan(bp, n_dst, n_src, elem_bytes, scatter=True)
     if contig and (n_src * elem_bytes) % 16:
         # 16-byte source vectors would straddle batch entries
         return _scalar_gather_plan(f, g, n_dst, n_src, elem_bytes, masked)
@@ -175,6 +186,49 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
                            "LEGO_MASKED": int(masked), "LEGO_UNROLL": unroll})
     return RemapPlan(runtime.KIND_GATHER, n_dst, n_src, elem_bytes, contig, masked, src, info,
                      f"contiguous={contig}, masked={masked}")
+
+
+def _mirrorable(src_layout, dst_layout) -> bool:
+    """Both sides are bijections with an inverse (no ExpandBy holes, no
+    injective-only layout), so the source -> destination map exists."""
+    for side in (src_layout, dst_layout):
+        if isinstance(side, lower.ExpandBy):
+            return False
+        if side is not None and getattr(lower._group(side), "injective", False):
+            return False
+    return src_layout is not None
+
+
+def _staged_plan(bp, n_dst, n_src, elem_bytes, scatter=False) -> RemapPlan:
+    """Box-staged remap (LEGO_KIND 5): one CTA per destination block of
+    bp.block elements with its source box staged through shared memory, or
+    (scatter) one CTA per source block landing in its destination box."""
+    v = 16 // elem_bytes
+    cells = bp.rows * bp.pitch
+    tab_t = "unsigned short" if cells <= 0xFFFF else "unsigned int"
+    body = codegen.constant("B", bp.block) + codegen.constant("R", bp.rows)
+    body += codegen.constant("C", bp.cols) + codegen.constant("PITCH", bp.pitch)
+    body += codegen.constant("SX", bp.sx) + codegen.constant("NSRC", n_src)
+    body += f"typedef {tab_t} tab_t;\n"
+    body += (f"__device__ __align__(16) const tab_t TAB[{bp.block}] = {{"
+             + ",".join(str(int(o)) for o in bp.offsets) + "};\n")
+    body += codegen.generate("base_of", [bp.q], {"b": bp.base}).source
+    lvec = (bp.cols * elem_bytes) % 16 == 0 and (bp.sx * elem_bytes) % 16 == 0
+    smem = -(-cells * elem_bytes // 16) * 16
+    free = runtime.ALIGN_SRC_FREE | runtime.ALIGN_DST_FREE
+    if scatter:
+        units, reserved = n_src // bp.block, free
+    else:
+        units = n_dst // bp.block
+        reserved = runtime.ALIGN_SRC_FREE | (0 if bp.vec_store else runtime.ALIGN_DST_FREE)
+    info = runtime.ProgramInfo(kind=runtime.KIND_STAGED, elem_bytes=elem_bytes, n=n_dst,
+                               units=units, unit_threads=256, block=256, smem_bytes=smem,
+                               reserved=reserved)
+    src = _assemble(body, {"LEGO_KIND": 5, "LEGO_ELEM": elem_bytes, "LEGO_LVEC": int(lvec),
+                           "LEGO_SVEC16": int((bp.pitch * elem_bytes) % 16 == 0),
+                           "LEGO_VSTORE": int(bp.vec_store), "LEGO_SCATTER": int(scatter)})
+    return RemapPlan(runtime.KIND_STAGED, n_dst, n_src, elem_bytes, False, False, src, info,
+                     ("source blocks into destination " if scatter else "") + repr(bp))
 
 
 def _scalar_gather_plan(f, g, n_dst, n_src, elem_bytes, masked) -> RemapPlan:
@@ -216,6 +270,9 @@ TRANSPOSE_MINB = int(os.environ.get("LEGO_TRANSPOSE_MINB", "1"))
 TILE_ORDER = os.environ.get("LEGO_TILE_ORDER", "block")
 # CTAs of the persistent transpose variant (2 resident CTAs x 148 SMs by default)
 PERSIST_CTAS = int(os.environ.get("LEGO_PERSIST_CTAS", str(2 * 148)))
+# box-staged gathers (staging.py, LEGO_KIND 5) for non-contiguous gathers whose
+# destination blocks each read one compact source box (0 disables)
+BOX_STAGING = int(os.environ.get("LEGO_BOX", "1"))
 # band tile order: 0 row-block major, 1 diagonal-block major, -1 = per direction
 BAND_ORDER = int(os.environ.get("LEGO_BAND_ORDER", "-1"))
 
@@ -286,7 +343,7 @@ def _scatter_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
 def _remap_program(src_layout, dst_layout, elem_bytes):
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, TRANSPOSE_VARIANT,
            BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB,
-           BAND_ROWS, BAND_DIAGS)
+           BAND_ROWS, BAND_DIAGS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE)
     plans = []
 
     def build():

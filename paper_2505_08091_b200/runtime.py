@@ -49,7 +49,7 @@ class ProgramInfo(ctypes.Structure):
                 ("reserved", ctypes.c_int32)]
 
 
-KIND_INDEX_MAP, KIND_GATHER, KIND_TRANSPOSE, KIND_BAND, KIND_SCATTER = 0, 1, 2, 3, 4
+KIND_INDEX_MAP, KIND_GATHER, KIND_TRANSPOSE, KIND_BAND, KIND_SCATTER, KIND_STAGED = 0, 1, 2, 3, 4, 5
 # lego_program_info.reserved flags (include/lego_b200.h): element-aligned buffers suffice
 ALIGN_SRC_FREE, ALIGN_DST_FREE = 1, 2
 
