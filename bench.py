@@ -418,7 +418,7 @@ def other_kernels(args, pk, world):
     del m4
     # SURVEY section 8(f) rows at scale (parity-tested in tests/): f1 multi-stage chain with an
     # in-tile GenP (Eq. (2) shape), f2 ExpandBy partial tiles, f4 injective scatter
-    def frow(name, layout, n_elems, direction, dtype=torch.int32, scatter=False):
+    def frow(name, layout, n_elems, direction, dtype=torch.int32, scatter=False, traffic_key=None):
         x = torch.arange(n_elems, device="cuda", dtype=torch.int64).to(dtype)
         src_l, dst_l = (None, layout) if direction == "to" else (layout, None)
         out = K.remap(x, src_l, dst_l)
@@ -426,17 +426,18 @@ def other_kernels(args, pk, world):
         plan = K.remap_plan(src_l, dst_l, x.element_size())
         # bytes: each source element read once, each written destination element once
         nbytes = (2 * x.numel() if scatter else x.numel() + out.numel()) * x.element_size()
-        hbm_entry(name, nbytes, fn, None, {"plan": repr(plan)})
+        hbm_entry(name, nbytes, fn, traffic_key, {"plan": repr(plan)})
         del x, out
     f1 = L.parse_layout("GroupBy([8192,8192]).OrderBy(RegP([128,64,128,64],[1,3,2,4]))"
                         ".OrderBy(RegP([128,128],[2,1]), GenP([64,64], antidiag))")
-    frow("f1_chain_tile_antidiag_8192_i32", f1, 8192 * 8192, "to")
+    frow("f1_chain_tile_antidiag_8192_i32", f1, 8192 * 8192, "to", traffic_key="remap_staged_f1_i32")
     f2 = L.parse_layout("ExpandBy([8000,8000],[8192,8192],"
                         "GroupBy([8192,8192]).OrderBy(RegP([128,64,128,64],[1,3,2,4])))")
     frow("f2_expand_partial_tiles_i32", f2, lower_size(f2), "from")
     even = L.GenP((1 << 26,), L.PermFn(lambda idx: idx[0] * 2, lambda idx: idx[0] * 2), None, name="even")
     f4 = L.GroupBy([1 << 26], orders=(L.OrderBy(even),), injective=True)
-    frow("f4_injective_even_scatter_i32", f4, 1 << 26, "to", scatter=True)
+    frow("f4_injective_even_scatter_i32", f4, 1 << 26, "to", scatter=True,
+         traffic_key="remap_scatter_f4_i32")
     # cfg4b: NW wavefront 16384^2 int32
     try:
         sim = torch.randint(-10, 11, (16384, 16384), device="cuda", dtype=torch.int32)

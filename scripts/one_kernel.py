@@ -43,6 +43,18 @@ elif name == "apply_map":
     g = L.parse_layout("GroupBy([16384,16384]).OrderBy(GenP([16384,16384], antidiag))")
     out = torch.empty(16384 * 16384, device="cuda", dtype=torch.int32)
     fn = lambda: K.inv_map(g, out=out)  # noqa: E731
+elif name == "staged":
+    g = L.parse_layout("GroupBy([8192,8192]).OrderBy(RegP([128,64,128,64],[1,3,2,4]))"
+                       ".OrderBy(RegP([128,128],[2,1]), GenP([64,64], antidiag))")
+    x = torch.arange(8192 * 8192, device="cuda", dtype=torch.int32)
+    y = torch.empty_like(x)
+    fn = lambda: K.remap(x, None, g, out=y)  # noqa: E731
+elif name == "scatter":
+    even = L.GenP((1 << 26,), L.PermFn(lambda idx: idx[0] * 2, lambda idx: idx[0] * 2), None, name="even")
+    g = L.GroupBy([1 << 26], orders=(L.OrderBy(even),), injective=True)
+    x = torch.arange(1 << 26, device="cuda", dtype=torch.int32)
+    y = K.remap(x, None, g)
+    fn = lambda: K.remap(x, None, g, out=y)  # noqa: E731
 else:
     raise SystemExit(f"unknown kernel {name}")
 for _ in range(reps):
