@@ -16,15 +16,15 @@
 //    order from an atomic ticket (a strip's left neighbour is always already
 //    running); a persistent grid of at most one CTA per SM;
 //  * four warp roles per CTA, one per SM sub-partition:
-//      warp 0  compute:  sweeps the strip anti-diagonally over 2x4 cell blocks
+//      warp 0  compute:  sweeps the strip anti-diagonally over 4x4 cell blocks
 //              -- lane j owns columns 4j..4j+3 and at step s computes rows
-//              2(s-j), 2(s-j)+1, i.e. each step is one anti-diagonal of the
-//              (row pairs x 32 lane-columns) grid, the LEGO antidiag order of
-//              the paper's NW kernel.  The two left
+//              4(s-j) .. 4(s-j)+3, i.e. each step is one anti-diagonal of the
+//              (row quads x 32 lane-columns) grid, the LEGO antidiag order of
+//              the paper's NW kernel.  The four left
 //              values arrive by one warp shuffle each; everything else is in
-//              registers or one 16-byte shared load;
+//              registers or 16-byte shared loads prefetched two steps ahead;
 //      warp 1  producer: cp.async-stages sim, 32 rows x 128 columns per
-//              block, into an 8-block ring (the compute warp overwrites each
+//              block, into a 12-block ring (the compute warp overwrites each
 //              sim row with its S' row in place);
 //      warp 2  boundary: polls the left strip's published last column
 //              (32-bit words in global memory, preset to a sentinel no

@@ -208,7 +208,7 @@ def _staged_plan(bp, n_dst, n_src, elem_bytes, scatter=False) -> RemapPlan:
     tab_t = "unsigned short" if cells <= 0xFFFF else "unsigned int"
     body = codegen.constant("B", bp.block) + codegen.constant("R", bp.rows)
     body += codegen.constant("C", bp.cols) + codegen.constant("PITCH", bp.pitch)
-    body += codegen.constant("SX", bp.sx) + codegen.constant("NSRC", n_src)
+    body += codegen.constant("SX", bp.sx)
     body += f"typedef {tab_t} tab_t;\n"
     body += (f"__device__ __align__(16) const tab_t TAB[{bp.block}] = {{"
              + ",".join(str(int(o)) for o in bp.offsets) + "};\n")
