@@ -73,6 +73,21 @@ template <> struct lego_elem<2> { typedef unsigned short t; };
 template <> struct lego_elem<4> { typedef unsigned int t; };
 template <> struct lego_elem<8> { typedef unsigned long long t; };
 
+#if LEGO_ROUTED
+// routed destinations (fused remap + all-to-all over peer memory, shard.py):
+// the kernel's dst argument is a device array of per-rank base pointers (the
+// peers' symmetric buffers, NVLink-mapped); destination element v of the
+// remap goes to buffer gen::route(v).peer at element offset .off.  The
+// planner proved that every aligned 16-byte destination vector stays in one
+// peer, contiguous and 16-byte aligned (kernels._routed_plan).
+static __device__ __forceinline__ unsigned char* lego_route(unsigned char* table, long long v, int elem) {
+    long long peer, off;
+    gen::route(v, peer, off);
+    unsigned char* base = reinterpret_cast<unsigned char* const*>(table)[peer];
+    return base + off * elem;
+}
+#endif
+
 // ---------------------------------------------------------------------------
 #if LEGO_KIND == 0
 // index maps: one thread per output element, int32 or int64 outputs.
@@ -212,7 +227,11 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
 #pragma unroll
     for (int u = 0; u < LEGO_UNROLL; ++u) {
         const long long q = base + (long long)u * blockDim.x;
+#if LEGO_ROUTED
+        if (q < nvec) lego_st16(lego_route(dst, q * LEGO_VEC, LEGO_ELEM), v[u]);
+#else
         if (q < nvec) lego_st16(d + q * 16, v[u]);
+#endif
     }
 }
 #endif  // LEGO_SCALAR
@@ -398,9 +417,16 @@ LEGO_GLOBAL void __launch_bounds__(256, LEGO_MINB) lego_remap(const unsigned cha
         if (t0 + u >= gen::TILES) break;
         lego_v16 cols[LEGO_V];
         lego_transpose(rows[u], cols);
+#if LEGO_ROUTED
+        const long long v0 = f0[u] + (long long)(yg * LEGO_V) * gen::DY + xg * LEGO_V;
+#pragma unroll
+        for (int c = 0; c < LEGO_V; ++c)
+            lego_st16(lego_route(dst, v0 + (long long)c * gen::DY, LEGO_ELEM), cols[c]);
+#else
         unsigned char* dp = d + (f0[u] + (long long)(yg * LEGO_V) * gen::DY + xg * LEGO_V) * LEGO_ELEM;
 #pragma unroll
         for (int c = 0; c < LEGO_V; ++c) lego_st16(dp + (long long)c * gen::DY * LEGO_ELEM, cols[c]);
+#endif
     }
 }
 #endif  // LEGO_SMEM

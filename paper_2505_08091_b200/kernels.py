@@ -32,7 +32,8 @@ from typing import Dict, Optional, Tuple
 
 from . import codegen, lower, runtime, staging
 from .errors import BijectivityViolation, ShapeMismatch, UnsupportedNode
-from .expr import Var
+from .expr import IntConst, Var, VarRange
+from .simplify import _lin_of
 
 CSRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc")
 _TEXT: Dict[str, str] = {}
@@ -113,9 +114,21 @@ class RemapPlan:
                 f"{self.detail})")
 
 
-def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
+class Route:
+    """Destination routing of a remap over several buffers: destination
+    element v goes to buffer ``peer(v)`` at element offset ``off(v)``.
+    ``fn(v: Var) -> (peer_expr, off_expr)`` builds both as LEGO index
+    expressions; ``key`` identifies the routing for the program cache."""
+
+    def __init__(self, world: int, fn, key):
+        self.world, self.fn, self.key = world, fn, key
+
+
+def plan_remap(src_layout, dst_layout, elem_bytes: int, route: Optional[Route] = None) -> RemapPlan:
     if elem_bytes not in (1, 2, 4, 8, 16):
         raise UnsupportedNode(f"element size {elem_bytes} not supported (1, 2, 4, 8 or 16 bytes)")
+    if route is not None:
+        return _routed_plan(src_layout, dst_layout, elem_bytes, route)
     band = _band_plan(src_layout, dst_layout, elem_bytes)
     if band is not None:
         return band
@@ -186,6 +199,55 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
                            "LEGO_MASKED": int(masked), "LEGO_UNROLL": unroll})
     return RemapPlan(runtime.KIND_GATHER, n_dst, n_src, elem_bytes, contig, masked, src, info,
                      f"contiguous={contig}, masked={masked}")
+
+
+def _routed_plan(src_layout, dst_layout, elem_bytes, route) -> RemapPlan:
+    """A gather or register transpose whose 16-byte destination vectors are
+    routed to peer buffers (remap_kernels.cuh LEGO_ROUTED).  Proves, for every
+    aligned vector v = V*q + k (k < V), that peer(v) == peer(V*q),
+    off(v) == off(V*q) + k and off(V*q) % V == 0, and 0 <= peer < world."""
+    f, g, n_dst, n_src = lower.gather_expr(src_layout, dst_layout)
+    vec = 16 // elem_bytes
+    peer_e, off_e = (lower.simplify(lower.as_expr(e)) for e in route.fn(f))
+    lo, hi = lower.value_range(g)
+    if n_dst % vec or lo < 0:
+        raise UnsupportedNode("routed remaps need whole 16-byte destination vectors and no masked reads")
+    q = Var("q", VarRange(0, n_dst // vec))
+    r = Var("r", VarRange(0, vec))
+    at = lambda e, x: lower.simplify(lower.substitute(e, {f.name: x}))  # noqa: E731
+    p0, o0 = at(peer_e, q * vec), at(off_e, q * vec)
+    same_peer = lower.simplify(at(peer_e, q * vec + r) - p0) == IntConst(0)
+    contiguous = lower.simplify(at(off_e, q * vec + r) - o0 - r) == IntConst(0)
+    lin = _lin_of(o0)
+    aligned = lin.const % vec == 0 and all(c % vec == 0 for c in lin.terms.values())
+    plo, phi = lower.value_range(peer_e)
+    if not (same_peer and contiguous and aligned and plo >= 0 and phi < route.world):
+        raise UnsupportedNode("routing must keep each 16-byte destination vector in one peer, "
+                              "contiguous and aligned")
+    body = codegen.constant("N", n_dst)
+    body += codegen.generate("route", [f], {"peer": peer_e, "off": off_e}).source
+    tp = lower.transpose_plan(g, f, n_dst, elem_bytes, 8, 4, TILE_ORDER)
+    if tp is not None:
+        body += codegen.constant("TILES", tp.tiles) + codegen.constant("SX", tp.sx)
+        body += codegen.constant("DY", tp.dy)
+        body += codegen.generate("origin", [tp.t], {"f0": tp.origin_f0, "s0": tp.origin_s0}).source
+        info = runtime.ProgramInfo(kind=runtime.KIND_TRANSPOSE, elem_bytes=elem_bytes, n=n_dst,
+                                   units=(tp.tiles + 7) // 8, unit_threads=32, block=256, smem_bytes=0)
+        src = _assemble(body, {"LEGO_KIND": 2, "LEGO_ELEM": elem_bytes, "LEGO_XMAJOR": 1,
+                               "LEGO_MINB": TRANSPOSE_MINB, "LEGO_ROUTED": 1})
+        return RemapPlan(runtime.KIND_TRANSPOSE, n_dst, n_src, elem_bytes, False, False, src, info,
+                         f"routed over {route.world} peers, tile {tp.tx}x{tp.ty} regT")
+    width = lower.contiguous_width(g, f, n_dst, widths=(vec,))
+    contig = width >= vec
+    body += codegen.generate("src_of", [f], {"s": g}, bounds={"s": (0, n_src - 1)}).source
+    units = (n_dst // vec + 1023) // 1024
+    info = runtime.ProgramInfo(kind=runtime.KIND_GATHER, elem_bytes=elem_bytes, n=n_dst,
+                               units=units, unit_threads=1, block=256, smem_bytes=0,
+                               reserved=0 if contig else runtime.ALIGN_SRC_FREE)
+    src = _assemble(body, {"LEGO_KIND": 1, "LEGO_ELEM": elem_bytes, "LEGO_CONTIG": int(contig),
+                           "LEGO_MASKED": 0, "LEGO_UNROLL": 4, "LEGO_ROUTED": 1})
+    return RemapPlan(runtime.KIND_GATHER, n_dst, n_src, elem_bytes, contig, False, src, info,
+                     f"routed over {route.world} peers, contiguous={contig}")
 
 
 def _mirrorable(src_layout, dst_layout) -> bool:
@@ -340,14 +402,15 @@ def _scatter_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
                      f"scatter into an injective layout, {n_dst} positions")
 
 
-def _remap_program(src_layout, dst_layout, elem_bytes):
-    key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, TRANSPOSE_VARIANT,
+def _remap_program(src_layout, dst_layout, elem_bytes, route=None):
+    key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes,
+           None if route is None else ("route", route.world, route.key), TRANSPOSE_VARIANT,
            BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB,
            BAND_ROWS, BAND_DIAGS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE)
     plans = []
 
     def build():
-        plans.append(plan_remap(src_layout, dst_layout, elem_bytes))
+        plans.append(plan_remap(src_layout, dst_layout, elem_bytes, route))
         return plans[0].source, plans[0].info
 
     prog = _program(key, build)
@@ -464,6 +527,31 @@ def remap(src, src_layout=None, dst_layout=None, *, out=None, stream=None):
         LAUNCHES[0] += 1
         done += b
     return out
+
+
+def remap_routed(src, src_layout, dst_layout, peers, route: Route, *, stream=None):
+    """One remap whose destination is spread over ``route.world`` buffers:
+    destination element v lands in buffer ``route.peer(v)`` at element offset
+    ``route.off(v)``.  ``peers`` is an int64 CUDA tensor holding the buffers'
+    device addresses -- for a cross-rank exchange, the NVLink-mapped
+    symmetric buffers of every rank, so the remap and the all-to-all are one
+    kernel (``shard.transpose_rows_fused``).  One matrix per call; the caller
+    orders the peers' reads after the stores (a barrier)."""
+    torch = _torch()
+    if not src.is_cuda or not peers.is_cuda or peers.dtype != torch.int64:
+        raise ShapeMismatch("remap_routed takes a CUDA source and an int64 CUDA peer table")
+    if peers.numel() != route.world:
+        raise ShapeMismatch(f"peer table has {peers.numel()} entries for {route.world} peers")
+    elem = src.element_size()
+    lower.check_pair(src_layout, dst_layout)
+    prog = _remap_program(src_layout, dst_layout, elem, route)
+    if src.numel() != prog.n_src:
+        raise ShapeMismatch(f"routed remap moves one layout of {prog.n_src} elements, got {src.numel()}")
+    src = src.contiguous()
+    runtime.check(runtime.lib().lego_remap(prog.handle, src.data_ptr(), peers.data_ptr(), 1,
+                                           prog.n_src, prog.n_dst, runtime.stream_handle(stream)),
+                  "lego_remap")
+    LAUNCHES[0] += 1
 
 
 def gather(src, layout, **kw):

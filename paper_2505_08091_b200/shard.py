@@ -10,7 +10,10 @@ has to cross shards:
 * :func:`transpose_rows` -- a *single* matrix whose rows are split across
   ranks, remapped into a layout that needs other ranks' rows (the
   column-major ``Col`` layout): one ``all_to_all_single`` of row-block x
-  column-block tiles, then each rank finishes with local LEGO remaps.
+  column-block tiles, then each rank finishes with local LEGO remaps;
+* :func:`transpose_rows_fused` -- the same result as one routed transpose
+  kernel per rank that stores straight into the other ranks' shards through
+  NVLink peer memory (torch symmetric memory), no NCCL in the data path.
 
 All functions take ``compute=`` so the host logic is testable on CPU with
 the ``gloo`` backend (tests/test_shard.py injects the oracle); the default
@@ -141,6 +144,58 @@ def transpose_rows(local_rows, n_rows: int, n_cols: int, *, group=None,
     tt = run(recv, None, t_layout)                          # (world, C*R), each C x R
     # place tiles side by side: out[c, q*R + r] = tt[q, c*R + r]
     return run(tt.reshape(-1), None, _sidebyside_layout(R, C, world)).reshape(C, world * R)
+
+
+def transpose_rows_fused(local_rows, n_rows: int, n_cols: int, *, group=None):
+    """:func:`transpose_rows` as ONE kernel per rank (B200/NVSwitch path).
+
+    Rank r's output shard lives in torch symmetric memory, so every rank can
+    store into every other rank's shard over NVLink.  Each rank runs one
+    routed register transpose of its local rows (``kernels.remap_routed``):
+    the 16-byte vectors of transposed row c go straight to rank c // C, at
+    the column offset of the sending rank's rows -- no staging tiles, no
+    NCCL all-to-all, the exchange overlaps the transpose tile by tile.  Two
+    device-side barriers order it: every shard is free before anyone
+    writes, and every store has landed before anyone reads.  Same result as
+    :func:`transpose_rows` (tests/test_shard.py checks the routing for every
+    rank on CPU; tests/test_gpu_kernels.py runs the routed kernel on a GPU
+    against per-rank buffers)."""
+    import torch
+    from torch.distributed import _symmetric_memory as symm
+    from . import kernels
+    dist = _dist()
+    world, rank = world_and_rank(group)
+    if n_rows % world or n_cols % world:
+        raise ShapeMismatch(f"{n_rows}x{n_cols} does not split over {world} ranks")
+    R, C = n_rows // world, n_cols // world
+    if local_rows.shape != (R, n_cols):
+        raise ShapeMismatch(f"local rows {tuple(local_rows.shape)} != {(R, n_cols)}")
+    out = symm.empty((C, n_rows), dtype=local_rows.dtype, device=local_rows.device)
+    handle = symm.rendezvous(out, group if group is not None else dist.group.WORLD)
+    peers = torch.tensor([int(p) for p in handle.buffer_ptrs], dtype=torch.int64,
+                         device=local_rows.device)
+    layout, route = fused_transpose_route(R, C, world, rank)
+    handle.barrier(channel=0)
+    kernels.remap_routed(local_rows.reshape(-1), None, layout, peers, route)
+    handle.barrier(channel=0)
+    return out
+
+
+def fused_transpose_route(R: int, C: int, world: int, rank: int):
+    """(local layout, kernels.Route) of :func:`transpose_rows_fused` on
+    ``rank``: the local (R x world*C) rows transposed to (world*C x R)
+    (position v = c*R + r), and v routed to rank c // C at element offset
+    (c % C) * (world*R) + rank*R + r of that rank's (C x world*R) shard."""
+    from .kernels import Route
+    from .layout import GroupBy, RegP
+    n_cols, n_rows = world * C, world * R
+    layout = GroupBy([R, n_cols]).order_by(RegP((R, n_cols), (2, 1)))
+
+    def fn(v):
+        c, r = v // R, v % R
+        return c // C, (c % C) * n_rows + rank * R + r
+
+    return layout, Route(world, fn, ("transpose_rows", R, C, world, rank))
 
 
 def _transpose_layouts(R, C, world):

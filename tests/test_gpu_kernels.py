@@ -115,3 +115,49 @@ def test_matmul_four_data_layouts(a_layout, b_layout, M, N, Kd, batch):
     denom = torch.clamp(ref.abs(), min=1e-2 * ref.abs().max().item())
     rel = ((c.double() - ref).abs() / denom).max().item()
     assert rel <= 1e-2, (a_layout, b_layout, M, N, Kd, rel)
+
+
+@pytest.mark.parametrize("dtype", [torch.int8, torch.int16, torch.int32, torch.int64])
+@pytest.mark.parametrize("world,R,C", [(4, 256, 128), (2, 64, 512)])
+def test_routed_transpose_into_peer_buffers(dtype, world, R, C):
+    """The fused remap + all-to-all kernel of shard.transpose_rows_fused, with
+    the `world` ranks' output shards emulated as separate buffers on one GPU:
+    every rank's routed transpose stores into all shards; together they hold
+    the transposed matrix, sharded by rows."""
+    from paper_2505_08091_b200 import shard
+    n_rows, n_cols = world * R, world * C
+    full = (torch.arange(n_rows * n_cols, device="cuda", dtype=torch.int64) * 2654435761 % 1000003)
+    full = full.to(dtype).reshape(n_rows, n_cols)
+    shards = [torch.full((C, n_rows), -1, dtype=dtype, device="cuda") for _ in range(world)]
+    peers = torch.tensor([t.data_ptr() for t in shards], dtype=torch.int64, device="cuda")
+    for rank in range(world):
+        layout, route = shard.fused_transpose_route(R, C, world, rank)
+        K.remap_routed(full[rank * R:(rank + 1) * R].reshape(-1), None, layout, peers, route)
+    torch.cuda.synchronize()
+    want = full.t().contiguous()
+    for q in range(world):
+        assert torch.equal(shards[q], want[q * C:(q + 1) * C]), q
+
+
+def test_transpose_rows_fused_single_rank_symmetric_memory(tmp_path):
+    """transpose_rows_fused end to end through torch symmetric memory on a
+    one-rank NCCL group (the only multi-process shape one GPU allows)."""
+    import torch.distributed as dist
+    from paper_2505_08091_b200 import shard
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised")
+    try:
+        dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", world_size=1, rank=0,
+                                device_id=torch.device("cuda:0"))
+    except Exception as exc:  # noqa: BLE001
+        pytest.skip(f"NCCL process group unavailable: {exc}")
+    try:
+        x = torch.randint(-1000, 1000, (512, 1024), device="cuda", dtype=torch.int32)
+        try:
+            out = shard.transpose_rows_fused(x, 512, 1024)
+        except (RuntimeError, NotImplementedError) as exc:
+            pytest.skip(f"symmetric memory unavailable: {exc}")
+        torch.cuda.synchronize()
+        assert torch.equal(out, x.t())
+    finally:
+        dist.destroy_process_group()

@@ -116,3 +116,43 @@ def test_single_process_defaults():
     x = torch.arange(16).reshape(4, 4)
     assert shard.plan(4).count == 4
     assert torch.equal(shard.local_slice(x), x)
+
+
+@pytest.mark.parametrize("world,R,C", [(2, 16, 8), (4, 8, 16), (8, 32, 8)])
+def test_fused_transpose_routing_every_rank(world, R, C):
+    """transpose_rows_fused's routing, evaluated for every rank and every
+    destination element: the union of all ranks' routed stores is exactly
+    the transposed matrix, sharded by rows, each element written once."""
+    from paper_2505_08091_b200 import lower, staging
+    from paper_2505_08091_b200.expr import Var, VarRange
+    n_rows, n_cols = world * R, world * C
+    full = np.arange(n_rows * n_cols, dtype=np.int64).reshape(n_rows, n_cols)
+    shards = np.full((world, C * n_rows), -1, dtype=np.int64)
+    for rank in range(world):
+        layout, route = shard.fused_transpose_route(R, C, world, rank)
+        f, g, n_dst, n_src = lower.gather_expr(None, layout)
+        assert (n_dst, n_src) == (R * n_cols, R * n_cols)
+        v = np.arange(n_dst)
+        src_idx = staging.eval_vec(g, {"f": v})                 # local source element of v
+        peer_e, off_e = route.fn(f)
+        peer = staging.eval_vec(lower.as_expr(peer_e), {"f": v})
+        off = staging.eval_vec(lower.as_expr(off_e), {"f": v})
+        local = full[rank * R:(rank + 1) * R].reshape(-1)
+        assert np.all(shards[peer, off] == -1)
+        shards[peer, off] = local[src_idx]
+    want = full.T.reshape(world, C * n_rows)
+    np.testing.assert_array_equal(shards, want)
+
+
+def test_fused_transpose_plan_proves_vector_routing():
+    """The planner accepts the routing (16-byte vectors stay in one peer,
+    contiguous, aligned) and picks the routed register transpose."""
+    from paper_2505_08091_b200 import kernels, runtime
+    layout, route = shard.fused_transpose_route(256, 128, 4, 1)
+    for elem in (2, 4):
+        p = kernels.plan_remap(None, layout, elem, route)
+        assert p.kind == runtime.KIND_TRANSPOSE and "routed over 4 peers" in p.detail
+    # a routing that splits vectors across peers is refused
+    bad = kernels.Route(2, lambda v: (v % 2, v // 2), ("bad",))
+    with pytest.raises(L.UnsupportedNode):
+        kernels.plan_remap(None, layout, 4, bad)
