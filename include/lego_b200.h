@@ -119,7 +119,11 @@ lego_status lego_check_bijective(lego_program p, uint32_t *hist, int64_t *violat
  * with g = src.apply o dst.inv compiled into the program, i.e. for every
  * logical index x: dst[dst.apply(x)] = src[src.apply(x)].  Strides are in
  * elements; buffers and batch strides must be 16-byte aligned on the sides
- * the program accesses with vectors (see lego_program_info.reserved). */
+ * the program accesses with vectors (see lego_program_info.reserved).
+ * Routed programs (built with a destination routing, e.g. the fused
+ * cross-rank transpose of shard.transpose_rows_fused): dst is a device array
+ * of per-peer base addresses and destination element f is stored at
+ * peer route.peer(f), element offset route.off(f); batch must be 1. */
 lego_status lego_remap(lego_program p, const void *src, void *dst, int64_t batch,
                        int64_t src_stride, int64_t dst_stride, void *stream);
 
