@@ -34,14 +34,17 @@ static __device__ __forceinline__ auto lego_fmod(A a, B b) -> decltype(a + b) {
 // MUFU square root (rel. error ~2^-22) land within 0.02 of sqrt(x) <= 46341;
 // the truncated root is off by at most one and one branch-free correction
 // step each way is exact
+// branch-free: the clamp is a max, and .ftz drops the denormal rescaling
+// (float(x) >= 1 or 0); checked exhaustively over [0, 2^31) and a sample of
+// negative arguments by scripts/micro/isqrt_exhaustive.cu
 static __device__ __forceinline__ int lego_isqrt32(int x) {
-    if (x <= 0) return 0;
+    const unsigned ux = (unsigned)max(x, 0);
     float fr;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(fr) : "f"((float)x));
-    int r = (int)fr;
-    r -= ((unsigned)r * (unsigned)r > (unsigned)x) ? 1 : 0;
-    r += ((unsigned)(r + 1) * (unsigned)(r + 1) <= (unsigned)x) ? 1 : 0;
-    return r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(fr) : "f"((float)ux));
+    unsigned r = (unsigned)fr;
+    r -= (r * r > ux) ? 1u : 0u;
+    r += ((r + 1u) * (r + 1u) <= ux) ? 1u : 0u;
+    return (int)r;
 }
 static __device__ __forceinline__ long long lego_isqrt64(long long x) {
     if (x <= 0) return 0;
