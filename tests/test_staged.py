@@ -176,3 +176,34 @@ def test_staged_f1_full_size():
                    ".OrderBy(RegP([128,128],[2,1]), GenP([64,64], antidiag))")
     want = O.inv_range(spec, first=12345 * 4096, count=3 * 4096)
     np.testing.assert_array_equal(fwd[12345 * 4096:12348 * 4096].cpu().numpy(), want)
+
+
+TWO = [
+    ("GroupBy([256,256]).OrderBy(RegP([4,64,4,64],[1,3,2,4])).OrderBy(RegP([4,4],[2,1]), GenP([64,64], antidiag))",
+     "GroupBy([256,256]).OrderBy(RegP([8,32,8,32],[1,3,2,4]))"),
+    ("GroupBy([256,256]).OrderBy(RegP([4,64,4,64],[1,3,2,4])).OrderBy(RegP([4,4],[2,1]), GenP([64,64], antidiag))",
+     "GroupBy([256,256]).OrderBy(Col(256,256))"),
+]
+
+
+@pytest.mark.parametrize("a,b", TWO)
+def test_two_layout_remaps_plan_staged(a, b):
+    la, lb = L.parse_layout(a), L.parse_layout(b)
+    for s_, d_ in ((la, lb), (lb, la)):
+        for elem in (2, 4):
+            assert K.plan_remap(s_, d_, elem).kind == runtime.KIND_STAGED
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("a,b", TWO)
+@pytest.mark.parametrize("elem", [2, 4])
+def test_two_layout_staged_remaps_vs_oracle(a, b, elem):
+    torch = _torch()
+    sa, sb = O.parse(a), O.parse(b)
+    la, lb = L.parse_layout(a), L.parse_layout(b)
+    n = O.size(sa)
+    host = (np.arange(2 * n, dtype=np.int64) * 40503 % 65521).astype(NP[elem]).reshape(2, n)
+    for (ls, ss), (ld, sd) in (((la, sa), (lb, sb)), ((lb, sb), (la, sa))):
+        got = K.remap(torch.from_numpy(host).cuda(), ls, ld).cpu().numpy()
+        for k in range(2):
+            np.testing.assert_array_equal(got[k], O.remap(host[k], ss, sd, dst_size=n))
