@@ -86,3 +86,31 @@ def random_expand(rng):
 def expand_corpus(count=24, seed=20261018):
     rng = random.Random(seed)
     return [random_expand(rng) for _ in range(count)]
+
+
+def _tile_perm(a, b, rng):
+    """A perm over an (a, b) tile: antidiag / rev2d when square, else a RegP/Row/Col."""
+    if a == b and rng.random() < 0.5:
+        return f"GenP([{a},{b}], {rng.choice(['antidiag', 'rev2d'])})"
+    return rng.choice([f"RegP([{a},{b}],[2,1])", f"Row({a},{b})", f"Col({b},{a})"])
+
+
+def tiled_chain(rng):
+    """SURVEY f1-style two-stage chain at up to 2^20 points: tile a (M x N)
+    matrix by (a x b), then reorder the tile grid and the in-tile elements."""
+    while True:
+        a = rng.choice([8, 16, 32, 64, 24, 48])
+        b = rng.choice([a, a, 16, 32, 64])
+        gm = rng.choice([2, 4, 8, 16, 3, 6])
+        gn = rng.choice([2, 4, 8, 16, 5])
+        if a * b * gm * gn <= 1 << 20:
+            break
+    M, N = a * gm, b * gn
+    text = (f"GroupBy([{M},{N}]).OrderBy(RegP([{gm},{a},{gn},{b}],[1,3,2,4]))"
+            f".OrderBy({_tile_perm(gm, gn, rng)}, {_tile_perm(a, b, rng)})")
+    return text
+
+
+def chain_corpus(count=16, seed=20261019):
+    rng = random.Random(seed)
+    return [tiled_chain(rng) for _ in range(count)]
