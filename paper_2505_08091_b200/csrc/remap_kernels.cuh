@@ -624,7 +624,98 @@ typedef lego_elem<LEGO_ELEM>::t lego_e;
 #define LEGO_BT 256                                    // threads per CTA
 struct alignas(sizeof(gen::tab_t) * LEGO_V) lego_tabv { gen::tab_t t[LEGO_V]; };
 
-#if LEGO_SCATTER
+// store phase of the gather form: destination block from the staged box
+static __device__ __forceinline__ void lego_box_store(const lego_e* box, lego_e* d, int tid) {
+#if LEGO_VSTORE
+    constexpr int NO = gen::B / LEGO_V;
+#pragma unroll 4
+    for (int k = tid; k < NO; k += LEGO_BT) {
+        const lego_tabv tv = reinterpret_cast<const lego_tabv*>(gen::TAB)[k];
+        union { lego_v16 v; lego_e e[LEGO_V]; } u;
+#pragma unroll
+        for (int e = 0; e < LEGO_V; ++e) u.e[e] = box[tv.t[e]];
+        lego_st16(reinterpret_cast<unsigned char*>(d + (long long)k * LEGO_V), u.v);
+    }
+#else
+#pragma unroll 8
+    for (int r = tid; r < gen::B; r += LEGO_BT) d[r] = box[gen::TAB[r]];
+#endif
+}
+
+#if LEGO_BULK
+// TMA-fed persistent form (the planner proved base(q)*E, SX*E, C*E and
+// PITCH*E are 16-byte multiples): each CTA walks blocks q = blockIdx.x,
+// + gridDim.x, ...; warp 0 issues the next block's R box rows as 1-D bulk
+// copies (cp.async.bulk, one per row, completing on an mbarrier with the
+// byte count) into the other of two box buffers while all warps permute and
+// store the current one.
+static __device__ __forceinline__ void lego_mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "LEGO_WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra LEGO_WAIT_%=;\n\t}" :: "r"(bar), "r"(parity) : "memory");
+}
+static __device__ __forceinline__ void lego_box_issue(const lego_e* s, long long q, unsigned box, unsigned bar,
+                                                      int lane) {
+    long long b0;
+    gen::base_of(q, b0);
+    constexpr unsigned ROWB = gen::C * LEGO_ELEM;
+    if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     :: "r"(bar), "r"((unsigned)(gen::R * ROWB)) : "memory");
+    __syncwarp();
+    for (int row = lane; row < gen::R; row += 32)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"(box + (unsigned)(row * gen::PITCH * LEGO_ELEM)),
+                        "l"(s + b0 + (long long)row * gen::SX), "r"(ROWB), "r"(bar) : "memory");
+}
+LEGO_GLOBAL void __launch_bounds__(LEGO_BT) lego_remap(const unsigned char* __restrict__ src,
+                                                       unsigned char* __restrict__ dst,
+                                                       long long src_stride, long long dst_stride) {
+    extern __shared__ __align__(128) unsigned char lego_smem[];
+    constexpr unsigned BOXB = (gen::R * gen::PITCH * LEGO_ELEM + 127) / 128 * 128;
+    const lego_e* s = reinterpret_cast<const lego_e*>(src) + (long long)blockIdx.y * src_stride;
+    lego_e* d = reinterpret_cast<lego_e*>(dst) + (long long)blockIdx.y * dst_stride;
+    const int tid = threadIdx.x;
+    const long long nblk = gen::N / gen::B;
+    const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(lego_smem));
+    const unsigned bar = sbase + 2 * BOXB;
+    if (((reinterpret_cast<unsigned long long>(s)) & 15) != 0) {
+        // unaligned source (batch stride or pointer): per-thread element loads
+        lego_e* box = reinterpret_cast<lego_e*>(lego_smem);
+        for (long long q = blockIdx.x; q < nblk; q += gridDim.x) {
+            long long b0;
+            gen::base_of(q, b0);
+            for (int k = tid; k < gen::R * gen::C; k += LEGO_BT) {
+                const int row = k / gen::C, col = k - row * gen::C;
+                box[row * gen::PITCH + col] = __ldg(s + b0 + (long long)row * gen::SX + col);
+            }
+            __syncthreads();
+            lego_box_store(box, d + q * gen::B, tid);
+            __syncthreads();
+        }
+        return;
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar + 8) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    long long q = blockIdx.x;
+    if (q >= nblk) return;
+    if (tid < 32) lego_box_issue(s, q, sbase, bar, tid);
+    for (int it = 0; q < nblk; q += gridDim.x, ++it) {
+        const int buf = it & 1;
+        const long long qn = q + gridDim.x;
+        // buffer buf^1 was released by the barrier that ended the previous iteration
+        if (qn < nblk && tid < 32) lego_box_issue(s, qn, sbase + (buf ^ 1) * BOXB, bar + 8 * (buf ^ 1), tid);
+        lego_mbar_wait(bar + 8 * buf, (it >> 1) & 1);
+        lego_box_store(reinterpret_cast<const lego_e*>(lego_smem + buf * BOXB), d + q * gen::B, tid);
+        __syncthreads();
+    }
+}
+#elif LEGO_SCATTER
 // mirrored form: source block q (B consecutive elements) lands in the
 // destination box at base(q) (R rows x C at stride SX): 16-byte loads of the
 // block, scattered into the box cells gen::TAB[r], then box rows stored
@@ -748,20 +839,7 @@ LEGO_GLOBAL void __launch_bounds__(LEGO_BT) lego_remap(const unsigned char* __re
         }
     }
     __syncthreads();
-#if LEGO_VSTORE
-    constexpr int NO = gen::B / LEGO_V;
-#pragma unroll 4
-    for (int k = tid; k < NO; k += LEGO_BT) {
-        const lego_tabv tv = reinterpret_cast<const lego_tabv*>(gen::TAB)[k];
-        union { lego_v16 v; lego_e e[LEGO_V]; } u;
-#pragma unroll
-        for (int e = 0; e < LEGO_V; ++e) u.e[e] = box[tv.t[e]];
-        lego_st16(reinterpret_cast<unsigned char*>(d + (long long)k * LEGO_V), u.v);
-    }
-#else
-#pragma unroll 8
-    for (int r = tid; r < gen::B; r += LEGO_BT) d[r] = box[gen::TAB[r]];
-#endif
+    lego_box_store(box, d, tid);
 }
 #endif  // LEGO_SCATTER
 #endif

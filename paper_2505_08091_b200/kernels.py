@@ -278,7 +278,19 @@ def _staged_plan(bp, n_dst, n_src, elem_bytes, scatter=False) -> RemapPlan:
     lvec = (bp.cols * elem_bytes) % 16 == 0 and (bp.sx * elem_bytes) % 16 == 0
     smem = -(-cells * elem_bytes // 16) * 16
     free = runtime.ALIGN_SRC_FREE | runtime.ALIGN_DST_FREE
-    if scatter:
+    # TMA-fed persistent form: every box row a 16-byte-aligned bulk copy
+    lin = _lin_of(bp.base)
+    bulk = (staging.BOX_BULK and not scatter and lvec and (bp.pitch * elem_bytes) % 16 == 0
+            and (lin.const * elem_bytes) % 16 == 0
+            and all((c * elem_bytes) % 16 == 0 for c in lin.terms.values()))
+    if bulk:
+        boxb = -(-cells * elem_bytes // 128) * 128
+        smem = 2 * boxb + 16
+        per_sm = max(1, min(8, (220 * 1024) // (smem + 1024)))
+        units = min(n_dst // bp.block, 148 * per_sm)
+        reserved = runtime.ALIGN_SRC_FREE | (0 if bp.vec_store else runtime.ALIGN_DST_FREE)
+        body += codegen.constant("N", n_dst)
+    elif scatter:
         units, reserved = n_src // bp.block, free
     else:
         units = n_dst // bp.block
@@ -288,9 +300,11 @@ def _staged_plan(bp, n_dst, n_src, elem_bytes, scatter=False) -> RemapPlan:
                                reserved=reserved)
     src = _assemble(body, {"LEGO_KIND": 5, "LEGO_ELEM": elem_bytes, "LEGO_LVEC": int(lvec),
                            "LEGO_SVEC16": int((bp.pitch * elem_bytes) % 16 == 0),
-                           "LEGO_VSTORE": int(bp.vec_store), "LEGO_SCATTER": int(scatter)})
+                           "LEGO_VSTORE": int(bp.vec_store), "LEGO_SCATTER": int(scatter),
+                           "LEGO_BULK": int(bulk)})
     return RemapPlan(runtime.KIND_STAGED, n_dst, n_src, elem_bytes, False, False, src, info,
-                     ("source blocks into destination " if scatter else "") + repr(bp))
+                     ("source blocks into destination " if scatter else "") + repr(bp)
+                     + (", TMA bulk rows, persistent" if bulk else ""))
 
 
 def _scalar_gather_plan(f, g, n_dst, n_src, elem_bytes, masked) -> RemapPlan:
@@ -406,7 +420,8 @@ def _remap_program(src_layout, dst_layout, elem_bytes, route=None):
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes,
            None if route is None else ("route", route.world, route.key), TRANSPOSE_VARIANT,
            BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB,
-           BAND_ROWS, BAND_DIAGS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE)
+           BAND_ROWS, BAND_DIAGS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE,
+           staging.BOX_BULK)
     plans = []
 
     def build():

@@ -60,6 +60,12 @@ BOX_SMEM = 48 * 1024
 # preferred destination bytes per block (16 KiB: 8 resident CTAs per SM keep
 # 128 KiB of loads in flight)
 BOX_TARGET = int(os.environ.get("LEGO_BOX_TARGET", str(16 * 1024)))
+# TMA-fed persistent staged kernel (cp.async.bulk box rows, double-buffered)
+# when the box rows are provably 16-byte aligned.  Off by default: on the f1
+# chain (256-byte box rows) it measured slower than the one-block-per-CTA
+# kernel (int32 5579 vs 6196 GB/s, bf16 4378 vs 5407; scripts/quick_staged.py)
+# -- 1-D bulk copies of a few hundred bytes do not amortise the TMA issue
+BOX_BULK = int(os.environ.get("LEGO_BOX_BULK", "0"))
 # smem-wavefront cost of one warp-wide global store in the store-mode model
 STG_WEIGHT = 8
 # store mode override for experiments: "" (cost model), "vec" or "scalar"

@@ -15,16 +15,16 @@ n = 8192 * 8192
 for dt in (torch.int32, torch.bfloat16, torch.uint8, torch.int64):
     x = torch.arange(n, device="cuda", dtype=torch.int64).to(dt)
     ref = None
-    for box, target, store in ((0, 16384, ""), (1, 16384, ""), (1, 16384, "vec"), (1, 16384, "scalar"),
-                               (1, 8192, ""), (1, 32768, "")):
-        K.BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE = box, target, store
+    for box, target, store, bulk in ((0, 16384, "", 0), (1, 16384, "", 0), (1, 16384, "", 1),
+                                     (1, 8192, "", 1), (1, 32768, "", 1), (1, 16384, "scalar", 1)):
+        K.BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE, staging.BOX_BULK = box, target, store, bulk
         out = torch.empty_like(x)
         ms = t(lambda: K.remap(x, None, f1, out=out))
         if ref is None:
             ref = out.clone()
         ok = torch.equal(out, ref)
         gbs = 2 * n * x.element_size() / (ms * 1e-3) / 1e9
-        print(f"{str(dt):15s} box={box} target={target:6d} store={store or 'auto':6s} {ms * 1e3:8.1f} us "
+        print(f"{str(dt):15s} box={box} bulk={bulk} target={target:6d} store={store or 'auto':6s} {ms * 1e3:8.1f} us "
               f"{gbs:7.1f} GB/s ok={ok}  {K.remap_plan(None, f1, x.element_size()).detail}", flush=True)
     for box in (0, 1):
         K.BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE = box, 16384, ""

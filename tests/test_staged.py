@@ -207,3 +207,22 @@ def test_two_layout_staged_remaps_vs_oracle(a, b, elem):
         got = K.remap(torch.from_numpy(host).cuda(), ls, ld).cpu().numpy()
         for k in range(2):
             np.testing.assert_array_equal(got[k], O.remap(host[k], ss, sd, dst_size=n))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("elem", [1, 2, 4, 8])
+def test_bulk_staged_variant_vs_oracle(elem, monkeypatch):
+    """The TMA-fed persistent variant (cp.async.bulk box rows, off by
+    default) stays bit-exact, aligned and unaligned sources."""
+    torch = _torch()
+    monkeypatch.setattr(staging, "BOX_BULK", 1)
+    text = STAGED[2]
+    g = L.parse_layout(text)
+    spec = O.parse(text)
+    n = O.logical_size(spec)
+    assert "TMA bulk" in K.remap_plan(None, g, elem).detail
+    host = (np.arange(n + 1, dtype=np.int64) * 2654435761 % 100003).astype(NP[elem])
+    dev = torch.from_numpy(host).cuda()
+    for view, h in ((dev[:n], host[:n]), (dev[1:], host[1:])):
+        got = K.remap(view.contiguous() if view.data_ptr() % 16 == 0 else view, None, g).cpu().numpy()
+        np.testing.assert_array_equal(got, O.remap(h, None, spec, dst_size=n))
