@@ -186,6 +186,8 @@ def cpu_remap_rate(target_seconds=10.0):
     host's cores over a bounded sample of the headline workload."""
     import numpy as np
     from oracle import oracle as O
+    # every host core (torchrun presets OMP_NUM_THREADS=1 for its workers)
+    O.set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
     spec = O.parse(HEADLINE_DSL)
     n = N * N
     src = (np.arange(n, dtype=np.int64) % 65536).astype(np.uint16)

@@ -294,6 +294,16 @@ int oracle_threads(void) {
 #endif
 }
 
+/* thread count for the parallel loops (launchers such as torchrun preset
+   OMP_NUM_THREADS=1; the timed CPU baseline wants every host core) */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* out[k] = apply(canon_unflatten(dims, first + k)); -1 marks an ExpandBy mask */
 int oracle_apply_range(const int64_t *desc, int64_t ndesc, int64_t first, int64_t count, int64_t *out) {
     layout_t L;

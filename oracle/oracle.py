@@ -67,12 +67,18 @@ def lib():
             fn.argtypes = [i32p, ctypes.c_int64, ctypes.c_int32, i32p]
             fn.restype = ctypes.c_int
         L.oracle_threads.restype = ctypes.c_int
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
+        L.oracle_set_threads.restype = None
         _lib = L
     return _lib
 
 
 def threads() -> int:
     return lib().oracle_threads()
+
+
+def set_threads(n: int) -> None:
+    lib().oracle_set_threads(int(n))
 
 
 # ---------------------------------------------------------------------------
