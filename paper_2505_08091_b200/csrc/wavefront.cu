@@ -220,7 +220,11 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, int4* ring_lan
     int left[RPS];
 #pragma unroll
     for (int q = 0; q < RPS; ++q) {
+#ifndef NW_ABL_NOSHFL
         const int sl = __shfl_up_sync(0xffffffffu, c.send[q], 1);
+#else
+        const int sl = c.send[q] + q;                   // ablation: no lane exchange (wrong results)
+#endif
         left[q] = lane == 0 ? lb[q] : sl;
     }
     const bool live = !GUARD || r0 >= 0;                // lanes start one step apart
