@@ -34,6 +34,12 @@ elif name == "gemm":
     b = torch.randn(8192, 8192, device="cuda").to(torch.bfloat16)
     c = torch.empty(8192, 8192, device="cuda", dtype=torch.bfloat16)
     fn = lambda: K.gemm(a, b, out=c)  # noqa: E731
+elif name.startswith("gemm_"):                      # gemm_<a layout><b layout>, e.g. gemm_colrow
+    al, bl = name[5:8], name[8:11]
+    a = torch.randn(8192, 8192, device="cuda").to(torch.bfloat16)
+    b = torch.randn(8192, 8192, device="cuda").to(torch.bfloat16)
+    c = torch.empty(8192, 8192, device="cuda", dtype=torch.bfloat16)
+    fn = lambda: K.matmul(a, b, a_layout=al, b_layout=bl, out=c)  # noqa: E731
 elif name.startswith("nw"):
     n = int(name[2:] or 16384)
     sim = torch.randint(-10, 11, (n, n), device="cuda", dtype=torch.int32)
