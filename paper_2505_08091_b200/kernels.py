@@ -25,7 +25,6 @@ No function here computes on the CPU; without the native library they raise
 from __future__ import annotations
 
 import ctypes
-import math
 import os
 import threading
 from typing import Dict, Optional, Tuple
