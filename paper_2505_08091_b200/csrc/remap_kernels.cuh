@@ -621,7 +621,9 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
 //               16-byte store), else one element per lane
 typedef lego_elem<LEGO_ELEM>::t lego_e;
 #define LEGO_V (16 / LEGO_ELEM)
+#ifndef LEGO_BT
 #define LEGO_BT 256                                    // threads per CTA
+#endif
 struct alignas(sizeof(gen::tab_t) * LEGO_V) lego_tabv { gen::tab_t t[LEGO_V]; };
 
 // store phase of the gather form: destination block from the staged box

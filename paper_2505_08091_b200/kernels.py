@@ -295,12 +295,13 @@ def _staged_plan(bp, n_dst, n_src, elem_bytes, scatter=False) -> RemapPlan:
         units = n_dst // bp.block
         reserved = runtime.ALIGN_SRC_FREE | (0 if bp.vec_store else runtime.ALIGN_DST_FREE)
     info = runtime.ProgramInfo(kind=runtime.KIND_STAGED, elem_bytes=elem_bytes, n=n_dst,
-                               units=units, unit_threads=256, block=256, smem_bytes=smem,
+                               units=units, unit_threads=staging.BOX_THREADS, block=staging.BOX_THREADS,
+                               smem_bytes=smem,
                                reserved=reserved)
     src = _assemble(body, {"LEGO_KIND": 5, "LEGO_ELEM": elem_bytes, "LEGO_LVEC": int(lvec),
                            "LEGO_SVEC16": int((bp.pitch * elem_bytes) % 16 == 0),
                            "LEGO_VSTORE": int(bp.vec_store), "LEGO_SCATTER": int(scatter),
-                           "LEGO_BULK": int(bulk)})
+                           "LEGO_BULK": int(bulk), "LEGO_BT": staging.BOX_THREADS})
     return RemapPlan(runtime.KIND_STAGED, n_dst, n_src, elem_bytes, False, False, src, info,
                      ("source blocks into destination " if scatter else "") + repr(bp)
                      + (", TMA bulk rows, persistent" if bulk else ""))
@@ -420,7 +421,7 @@ def _remap_program(src_layout, dst_layout, elem_bytes, route=None):
            None if route is None else ("route", route.world, route.key), TRANSPOSE_VARIANT,
            BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB,
            BAND_ROWS, BAND_DIAGS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE,
-           staging.BOX_BULK)
+           staging.BOX_BULK, staging.BOX_THREADS)
     plans = []
 
     def build():

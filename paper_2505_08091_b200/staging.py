@@ -66,6 +66,8 @@ BOX_TARGET = int(os.environ.get("LEGO_BOX_TARGET", str(16 * 1024)))
 # kernel (int32 5579 vs 6196 GB/s, bf16 4378 vs 5407; scripts/quick_staged.py)
 # -- 1-D bulk copies of a few hundred bytes do not amortise the TMA issue
 BOX_BULK = int(os.environ.get("LEGO_BOX_BULK", "0"))
+# threads per CTA of the staged kernel
+BOX_THREADS = int(os.environ.get("LEGO_BOX_THREADS", "256"))
 # smem-wavefront cost of one warp-wide global store in the store-mode model
 STG_WEIGHT = 8
 # store mode override for experiments: "" (cost model), "vec" or "scalar"
