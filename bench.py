@@ -435,7 +435,7 @@ def other_kernels(args, pk, world):
     frow("f1_chain_tile_antidiag_8192_i32", f1, 8192 * 8192, "to", traffic_key="remap_staged_f1_i32")
     f2 = L.parse_layout("ExpandBy([8000,8000],[8192,8192],"
                         "GroupBy([8192,8192]).OrderBy(RegP([128,64,128,64],[1,3,2,4])))")
-    frow("f2_expand_partial_tiles_i32", f2, lower_size(f2), "from")
+    frow("f2_expand_partial_tiles_i32", f2, lower_size(f2), "from", traffic_key="remap_expand_f2_i32")
     even = L.GenP((1 << 26,), L.PermFn(lambda idx: idx[0] * 2, lambda idx: idx[0] * 2), None, name="even")
     f4 = L.GroupBy([1 << 26], orders=(L.OrderBy(even),), injective=True)
     frow("f4_injective_even_scatter_i32", f4, 1 << 26, "to", scatter=True,

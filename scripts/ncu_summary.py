@@ -25,11 +25,12 @@ ALGO = {  # algorithmic bytes per launch of the captured workload (scripts/one_k
     "transpose": 2 * 16384 * 16384 * 2, "gather": 2 * 8 * 4096 * 4096 * 4,
     "band": 2 * 16384 * 16384 * 4, "softmax": 2 * 8192 * 8192 * 4,
     "nw": 16384 * 16384 * 4 + 16385 * 16385 * 4, "apply_map": 16384 * 16384 * 4,
-    "staged": 2 * 8192 * 8192 * 4, "scatter": 2 * (1 << 26) * 4,
+    "staged": 2 * 8192 * 8192 * 4, "scatter": 2 * (1 << 26) * 4, "expand": (8192 * 8192 + 8000 * 8000) * 4,
 }
 KEYS = {"transpose": "remap_transpose_bf16", "gather": "remap_gather_fp32", "band": "remap_antidiag_i32",
         "softmax": "softmax_fp32", "nw": "nw_wavefront_i32", "apply_map": "inv_map_antidiag_i32",
-        "gemm": "gemm_bf16", "staged": "remap_staged_f1_i32", "scatter": "remap_scatter_f4_i32"}
+        "gemm": "gemm_bf16", "staged": "remap_staged_f1_i32", "scatter": "remap_scatter_f4_i32",
+        "expand": "remap_expand_f2_i32"}
 
 
 def raw(rep):
@@ -54,7 +55,7 @@ try:
         traffic = json.load(fh)
 except (OSError, ValueError):
     traffic = {}
-for name in ["transpose", "gather", "band", "softmax", "gemm", "nw", "apply_map", "staged", "scatter"]:
+for name in ["transpose", "gather", "band", "softmax", "gemm", "nw", "apply_map", "staged", "scatter", "expand"]:
     rep = os.path.join(SRC, f"prof_{name}.ncu-rep")
     if not os.path.exists(rep):
         continue

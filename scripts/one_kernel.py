@@ -55,6 +55,12 @@ elif name == "staged":
     x = torch.arange(8192 * 8192, device="cuda", dtype=torch.int32)
     y = torch.empty_like(x)
     fn = lambda: K.remap(x, None, g, out=y)  # noqa: E731
+elif name == "expand":
+    g = L.parse_layout("ExpandBy([8000,8000],[8192,8192],"
+                       "GroupBy([8192,8192]).OrderBy(RegP([128,64,128,64],[1,3,2,4])))")
+    x = torch.arange(8000 * 8000, device="cuda", dtype=torch.int32)     # the physical buffer
+    y = K.remap(x, g, None)
+    fn = lambda: K.remap(x, g, None, out=y)  # noqa: E731
 elif name == "scatter":
     even = L.GenP((1 << 26,), L.PermFn(lambda idx: idx[0] * 2, lambda idx: idx[0] * 2), None, name="even")
     g = L.GroupBy([1 << 26], orders=(L.OrderBy(even),), injective=True)
