@@ -53,8 +53,10 @@ from .expr import (
 )
 from .simplify import Lin, _build, _lin_of, simplify
 
-# block sizes tried, largest first (elements of the destination)
+# block sizes tried (elements of the destination): the largest and smallest
 BLOCKS = (16384, 8192, 4096, 2048, 1024, 512, 256)
+# most block sizes tried per plan (each costs one simplification)
+MAX_BLOCKS = 16
 # shared-memory budget of one box (bytes)
 BOX_SMEM = 48 * 1024
 # preferred destination bytes per block (16 KiB: 8 resident CTAs per SM keep
@@ -337,8 +339,12 @@ def box_plan(g: Expr, f: Var, n_dst: int, n_src: int, elem_bytes: int) -> Option
     v = 16 // elem_bytes
     # blocks whose destination bytes fit BOX_TARGET first (largest first),
     # then larger ones (smallest first) up to the shared-memory budget
-    fits = [b for b in BLOCKS if b * elem_bytes <= BOX_TARGET]
-    order = fits + sorted(b for b in BLOCKS if b * elem_bytes > BOX_TARGET)
+    # candidates: every multiple of 32 in [256, 16384] dividing n_dst (tiles of
+    # 24 x 16 or 48 x 48 elements give blocks like 384 or 2304), at most
+    # MAX_BLOCKS of them
+    cands = [b for b in range(BLOCKS[-1], BLOCKS[0] + 1, 32) if n_dst % b == 0]
+    fits = sorted((b for b in cands if b * elem_bytes <= BOX_TARGET), reverse=True)
+    order = (fits + sorted(b for b in cands if b * elem_bytes > BOX_TARGET))[:MAX_BLOCKS]
     for block in order:
         if n_dst % block or block > n_dst:
             continue
