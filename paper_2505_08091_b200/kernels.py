@@ -557,6 +557,8 @@ def remap_routed(src, src_layout, dst_layout, peers, route: Route, *, stream=Non
         raise ShapeMismatch("remap_routed takes a CUDA source and an int64 CUDA peer table")
     if peers.numel() != route.world:
         raise ShapeMismatch(f"peer table has {peers.numel()} entries for {route.world} peers")
+    if peers.device != src.device:
+        raise ShapeMismatch("the peer table must live on the source's device")
     elem = src.element_size()
     lower.check_pair(src_layout, dst_layout)
     prog = _remap_program(src_layout, dst_layout, elem, route)
