@@ -226,3 +226,28 @@ def test_bulk_staged_variant_vs_oracle(elem, monkeypatch):
     for view, h in ((dev[:n], host[:n]), (dev[1:], host[1:])):
         got = K.remap(view.contiguous() if view.data_ptr() % 16 == 0 else view, None, g).cpu().numpy()
         np.testing.assert_array_equal(got, O.remap(h, None, spec, dst_size=n))
+
+
+@pytest.mark.gpu
+def test_staged_beyond_int32_positions():
+    """A staged layout with more than 2^31 positions (int8, 46400^2): 64-bit
+    block origins; sampled positions against the scalar layout API, and the
+    size-independent round trip through the mirrored kernel."""
+    torch = _torch()
+    text = ("GroupBy([46400,46400]).OrderBy(RegP([725,64,725,64],[1,3,2,4]))"
+            ".OrderBy(RegP([725,725],[2,1]), GenP([64,64], antidiag))")
+    g = L.parse_layout(text)
+    assert K.remap_plan(None, g, 1).kind == runtime.KIND_STAGED
+    n = 46400
+    assert n * n > 2 ** 31
+    x = torch.randint(-128, 128, (n * n,), dtype=torch.int8, device="cuda")
+    y = K.remap(x, None, g)
+    rng = np.random.default_rng(7)
+    ij = rng.integers(0, n, size=(2000, 2))
+    pos = torch.tensor([g.apply((int(i), int(j))) for i, j in ij], device="cuda")
+    flat = torch.tensor([int(i) * n + int(j) for i, j in ij], device="cuda")
+    assert torch.equal(y[pos], x[flat])
+    back = K.remap(y, g, None)
+    assert torch.equal(back, x)
+    del x, y, back
+    torch.cuda.empty_cache()
