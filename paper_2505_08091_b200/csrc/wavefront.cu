@@ -58,7 +58,10 @@ constexpr int RPS = NW_RPS;
 constexpr int STEPS = BLK / RPS;                     // compute steps per block
 constexpr int BLAG = (31 + STEPS - 1) / STEPS + 1;   // lane 31 completes block k before block k+BLAG starts
 constexpr int DRAIN = (31 + STEPS - 1) / STEPS;      // extra blocks cover lane 31's 31-step lag
-constexpr int GRP = 8 / RPS;                         // boundary readiness checked every GRP steps
+#ifndef NW_GRP
+#define NW_GRP (16 / NW_RPS)                         // measured: 4 steps 1068 us, 2 steps 1075, 1 step 1126 (n = 16384)
+#endif
+constexpr int GRP = NW_GRP;                          // boundary readiness checked every GRP steps
 constexpr int NSLOT = 12;                            // ring blocks
 constexpr int RING_ROWS = NSLOT * BLK;               // 384
 constexpr int BND_ROWS = 256;                        // boundary ring (rows)
