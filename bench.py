@@ -203,7 +203,7 @@ def cpu_remap_rate(target_seconds=10.0):
     dt = time.perf_counter() - t0
     gbs = 2 * 2 * count / dt / 1e9
     return {"value": round(gbs, 3), "unit": "GB/s", "cores": O.threads(), "kind": "port",
-            "sample": f"{count} of {n} elements ({count // N} rows) of the headline remap, "
+            "sample": f"{count} of {n} 16-bit elements ({count // N} rows; bf16 moved as uint16 bit patterns) of the headline remap, "
                       f"oracle/lego_oracle.c per-element apply (reference layout.py:313) "
                       f"with {O.threads()} OpenMP threads, {dt:.2f} s"}
 
@@ -224,7 +224,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(2 * 2 * N * N / (value * 1e9) * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic", "config": {"workload": WORKLOAD, "per_gpu_matrices": 1},
             "cpu_baseline": {**base, "value": round(value, 3)},
             "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
