@@ -67,7 +67,7 @@ constexpr int RING_ROWS = NSLOT * BLK;               // 384
 constexpr int BND_ROWS = 256;                        // boundary ring (rows)
 constexpr int BND_GROUPS = BND_ROWS / BLK;
 constexpr int ROW_BYTES = STRIP * 4;                 // 512
-constexpr int RING_BYTES = RING_ROWS * ROW_BYTES;    // 128 KiB
+constexpr int RING_BYTES = RING_ROWS * ROW_BYTES;    // 192 KiB
 constexpr int BND_BYTES = BND_ROWS * 4;
 constexpr int MBAR_BYTES = NSLOT * 8;
 constexpr int CTRL_BYTES = 64;
