@@ -599,6 +599,52 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
             unsigned char* stg = epi_stage + (warp - 2) * C_::EPI_BYTES;
             const uint32_t taddr = tmem_base + acc * ACC_COLS + half * EPI_COLS +
                                    (static_cast<uint32_t>(quarter * 32) << 16);
+#ifndef LEGO_GEMM_EARLY_RELEASE
+#define LEGO_GEMM_EARLY_RELEASE 1
+#endif
+#if LEGO_GEMM_EARLY_RELEASE
+            // drain the whole half into registers as packed bf16 pairs (128 words),
+            // release the TMEM columns to the MMA warp, then stage and store: the
+            // next tile's MMAs into this half overlap this tile's global stores
+            {
+                uint32_t pk[EPI_COLS / 2];
+#pragma unroll
+                for (int c = 0; c < EPI_COLS; c += 32 * EPI_CHUNKS) {
+                    uint32_t v[EPI_CHUNKS][32];
+#pragma unroll
+                    for (int h2 = 0; h2 < EPI_CHUNKS; ++h2) tmem_ld32(taddr + c + 32 * h2, v[h2]);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int h2 = 0; h2 < EPI_CHUNKS; ++h2)
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            pk[(c + 32 * h2) / 2 + j] = pack_bf16(__uint_as_float(v[h2][2 * j]),
+                                                                  __uint_as_float(v[h2][2 * j + 1]));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8u * (NH == 2 ? half : acc));
+#pragma unroll
+                for (int c = 0; c < EPI_COLS; c += 32) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 o = make_uint4(pk[c / 2 + 4 * q + 0], pk[c / 2 + 4 * q + 1],
+                                                   pk[c / 2 + 4 * q + 2], pk[c / 2 + 4 * q + 3]);
+                        *reinterpret_cast<uint4*>(stg + lane * 64 + 16 * (q ^ ((lane >> 1) & 3))) = o;
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int r = 8 * q + (lane >> 2), cq = lane & 3;
+                        const uint4 o = *reinterpret_cast<const uint4*>(stg + r * 64 + 16 * (cq ^ ((r >> 1) & 3)));
+                        const int gcol = nb * BN + half * EPI_COLS + c + 8 * cq;     // N % 8 == 0
+                        if (row0 + r < M && gcol < N)
+                            *reinterpret_cast<uint4*>(cbase + static_cast<size_t>(r) * N + c + 8 * cq) = o;
+                    }
+                    __syncwarp();
+                }
+            }
+#else
 #pragma unroll 1
 #ifdef LEGO_GEMM_ABL_NOEPI
             if (M < 0)                                          // ablation: skip the epilogue body
@@ -635,6 +681,7 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8u * (NH == 2 ? half : acc));
+#endif
         }
     }
     tc_fence_before();
