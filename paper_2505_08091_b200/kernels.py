@@ -271,7 +271,7 @@ def _staged_plan(bp, n_dst, n_src, elem_bytes, scatter=False) -> RemapPlan:
     body += codegen.constant("C", bp.cols) + codegen.constant("PITCH", bp.pitch)
     body += codegen.constant("SX", bp.sx)
     body += f"typedef {tab_t} tab_t;\n"
-    body += (f"__device__ __align__(16) const tab_t TAB[{bp.block}] = {{"
+    body += (f"__device__ __align__(32) const tab_t TAB[{bp.block}] = {{"
              + ",".join(str(int(o)) for o in bp.offsets) + "};\n")
     body += codegen.generate("base_of", [bp.q], {"b": bp.base}).source
     lvec = (bp.cols * elem_bytes) % 16 == 0 and (bp.sx * elem_bytes) % 16 == 0
