@@ -381,7 +381,10 @@ LEGO_GLOBAL void __launch_bounds__(256, 2) lego_remap(const unsigned char* __res
     }
 }
 #else
-LEGO_GLOBAL void __launch_bounds__(256, LEGO_MINB) lego_remap(const unsigned char* __restrict__ src,
+#ifndef LEGO_TBLOCK
+#define LEGO_TBLOCK 256
+#endif
+LEGO_GLOBAL void __launch_bounds__(LEGO_TBLOCK, LEGO_MINB) lego_remap(const unsigned char* __restrict__ src,
                                                    unsigned char* __restrict__ dst,
                                                    long long src_stride, long long dst_stride) {
     // LEGO_TPW warp tiles per warp: every tile's loads are issued before the

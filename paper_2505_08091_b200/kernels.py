@@ -153,7 +153,7 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int, route: Optional[Route] =
             body += codegen.constant("SX", tp.sx) + codegen.constant("DY", tp.dy)
             body += codegen.generate("origin", [tp.t], {"f0": tp.origin_f0,
                                                         "s0": tp.origin_s0}).source
-            warps = 4 if smem_variant else 8
+            warps = 4 if smem_variant else (TRANSPOSE_WARPS or _TRANSPOSE_WARPS_BY_ELEM[elem_bytes])
             v = 16 // elem_bytes
             smem = warps * 8 * v * 8 * 16 if smem_variant else 0
             per_cta = warps * tpw
@@ -166,7 +166,7 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int, route: Optional[Route] =
             src = _assemble(body, {"LEGO_KIND": 2, "LEGO_ELEM": elem_bytes,
                                    "LEGO_SMEM": int(smem_variant), "LEGO_TPW": tpw,
                                    "LEGO_PERSIST": int(persist), "LEGO_XMAJOR": int(xmajor),
-                                   "LEGO_MINB": TRANSPOSE_MINB})
+                                   "LEGO_MINB": TRANSPOSE_MINB, "LEGO_TBLOCK": 32 * warps})
             return RemapPlan(runtime.KIND_TRANSPOSE, n_dst, n_src, elem_bytes, False, False, src,
                              info, f"tile {tp.tx}x{tp.ty} {variant}, SX={tp.sx}, DY={tp.dy}")
     width = 1 if masked else lower.contiguous_width(g, f, n_dst, widths=(vec,))
@@ -340,6 +340,11 @@ TRANSPOSE_VARIANT = os.environ.get("LEGO_TRANSPOSE", "")
 # headline transpose and +1.4% on the tiled gather; scripts/quick_hints.py)
 LOAD_HINT = int(os.environ.get("LEGO_LDV", "1"))
 STORE_HINT = int(os.environ.get("LEGO_STV", "0"))
+# warps per CTA of the register transpose; 0 = measured default per element
+# size (scripts/quick_transpose_warps2.py, 16384^2 on B200: bf16 12 warps
+# 170.0 us vs 8 warps 172.7; fp32 16 warps; int64 8)
+TRANSPOSE_WARPS = int(os.environ.get("LEGO_TRANSPOSE_WARPS", "0"))
+_TRANSPOSE_WARPS_BY_ELEM = {1: 8, 2: 12, 4: 16, 8: 8, 16: 8}
 # minimum resident CTAs per SM requested for the register transpose (register cap)
 TRANSPOSE_MINB = int(os.environ.get("LEGO_TRANSPOSE_MINB", "1"))
 # warp-tile walk order of the transpose ("x", "y" or "block", see lower.transpose_plan)
@@ -420,7 +425,7 @@ def _remap_program(src_layout, dst_layout, elem_bytes, route=None):
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes,
            None if route is None else ("route", route.world, route.key), TRANSPOSE_VARIANT,
            BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB,
-           BAND_ROWS, BAND_DIAGS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE,
+           BAND_ROWS, BAND_DIAGS, TRANSPOSE_WARPS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE,
            staging.BOX_BULK, staging.BOX_THREADS)
     plans = []
 
