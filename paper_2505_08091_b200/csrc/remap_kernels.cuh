@@ -458,7 +458,10 @@ typedef lego_elem<LEGO_ELEM>::t lego_e;
 #define BK LEGO_BK                                     // diagonals per band tile (multiple of 32, <= 256)
 // 32-bit index arithmetic: the planner only selects this kernel when n*n < 2^31
 
-LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
+#ifndef LEGO_BW
+#define LEGO_BW 8                                      // warps per CTA
+#endif
+LEGO_GLOBAL void __launch_bounds__(32 * LEGO_BW) lego_remap(const unsigned char* __restrict__ src,
                                                    unsigned char* __restrict__ dst,
                                                    long long src_stride, long long dst_stride) {
     __shared__ lego_e tile[BR][BK + 1];
@@ -483,8 +486,8 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
     if (t0 > i0 + BR - 1 + n - 1) return;             // band right of the matrix
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // base position of each diagonal's run: pos(i, t-i) = base_t + i
-    if (threadIdx.x < BK) {
-        const int t = t0 + threadIdx.x;
+    for (int kk = threadIdx.x; kk < BK; kk += 32 * LEGO_BW) {
+        const int t = t0 + kk;
         int iv = max(t - (n - 1), i0);
         int b = -1;
         if (t <= 2 * n - 2 && iv <= t && iv < i0 + BR) {
@@ -492,15 +495,15 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
             gen::pos_of((long long)iv * n + (t - iv), p);
             b = (int)p - iv;
         }
-        run_base[threadIdx.x] = b;
+        run_base[kk] = b;
     }
-    constexpr int RPW = BR / 8;                        // rows (or diagonals) per warp
+    constexpr int RPW = BR / LEGO_BW;                  // rows per warp
 #if LEGO_DIR == 0
     {   // rows: BK consecutive elements of row i from column t0 - i; all loads first
         lego_e v[RPW][BK / 32];
 #pragma unroll
         for (int q = 0; q < RPW; ++q) {
-            const int i = i0 + warp + 8 * q;
+            const int i = i0 + warp + LEGO_BW * q;
             const int j0 = t0 - i;
             const lego_e* row = s + i * n;
 #pragma unroll
@@ -512,13 +515,13 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
 #pragma unroll
         for (int q = 0; q < RPW; ++q)
 #pragma unroll
-            for (int h = 0; h < BK / 32; ++h) tile[warp + 8 * q][32 * h + lane] = v[q][h];
+            for (int h = 0; h < BK / 32; ++h) tile[warp + LEGO_BW * q][32 * h + lane] = v[q][h];
     }
     __syncthreads();
     // diagonals: BR consecutive positions base_t + i
 #pragma unroll
-    for (int q = 0; q < BK / 8; ++q) {
-        const int k = warp + 8 * q;
+    for (int q = 0; q < BK / LEGO_BW; ++q) {
+        const int k = warp + LEGO_BW * q;
         const int t = t0 + k;
         const int b = run_base[k];
         if (b < 0) continue;
@@ -531,10 +534,10 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
 #else
     __syncthreads();
     {
-        lego_e v[BK / 8][BR / 32];
+        lego_e v[BK / LEGO_BW][BR / 32];
 #pragma unroll
-        for (int q = 0; q < BK / 8; ++q) {
-            const int k = warp + 8 * q;
+        for (int q = 0; q < BK / LEGO_BW; ++q) {
+            const int k = warp + LEGO_BW * q;
             const int t = t0 + k;
             const int b = run_base[k];
 #pragma unroll
@@ -544,20 +547,20 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
             }
         }
 #pragma unroll
-        for (int q = 0; q < BK / 8; ++q)
+        for (int q = 0; q < BK / LEGO_BW; ++q)
 #pragma unroll
-            for (int h = 0; h < BR / 32; ++h) tile[32 * h + lane][warp + 8 * q] = v[q][h];
+            for (int h = 0; h < BR / 32; ++h) tile[32 * h + lane][warp + LEGO_BW * q] = v[q][h];
     }
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < RPW; ++q) {
-        const int i = i0 + warp + 8 * q;
+        const int i = i0 + warp + LEGO_BW * q;
         const int j0 = t0 - i;
         lego_e* row = d + i * n;
 #pragma unroll
         for (int h = 0; h < BK / 32; ++h) {
             const int j = j0 + 32 * h + lane;
-            if ((unsigned)j < (unsigned)n) row[j] = tile[warp + 8 * q][32 * h + lane];
+            if ((unsigned)j < (unsigned)n) row[j] = tile[warp + LEGO_BW * q][32 * h + lane];
         }
     }
 #endif

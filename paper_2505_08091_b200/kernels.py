@@ -354,6 +354,8 @@ PERSIST_CTAS = int(os.environ.get("LEGO_PERSIST_CTAS", str(2 * 148)))
 # box-staged gathers (staging.py, LEGO_KIND 5) for non-contiguous gathers whose
 # destination blocks each read one compact source box (0 disables)
 BOX_STAGING = int(os.environ.get("LEGO_BOX", "1"))
+# warps per band CTA (BR and BK must be multiples of it)
+BAND_WARPS = int(os.environ.get("LEGO_BAND_WARPS", "8"))
 # band tile order: 0 row-block major, 1 diagonal-block major, -1 = per direction
 BAND_ORDER = int(os.environ.get("LEGO_BAND_ORDER", "-1"))
 
@@ -387,11 +389,12 @@ def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
         units = (n // br) * kblocks
     else:
         units = ((2 * n - 1 + bk - 1) // bk) * (n // br)
+    bw = BAND_WARPS
     info = runtime.ProgramInfo(kind=runtime.KIND_BAND, elem_bytes=elem_bytes, n=n * n, units=units,
-                               unit_threads=256, block=256, smem_bytes=0,
+                               unit_threads=32 * bw, block=32 * bw, smem_bytes=0,
                                reserved=runtime.ALIGN_SRC_FREE | runtime.ALIGN_DST_FREE)
     src = _assemble(body, {"LEGO_KIND": 3, "LEGO_ELEM": elem_bytes, "LEGO_DIR": direction,
-                           "LEGO_BAND_ORDER": order, "LEGO_BR": br, "LEGO_BK": bk})
+                           "LEGO_BAND_ORDER": order, "LEGO_BR": br, "LEGO_BK": bk, "LEGO_BW": bw})
     return RemapPlan(runtime.KIND_BAND, n * n, n * n, elem_bytes, False, False, src, info,
                      f"band {br} rows x {bk} diagonals, order {order}, "
                      f"{'scatter' if direction == 0 else 'gather'}")
@@ -425,7 +428,7 @@ def _remap_program(src_layout, dst_layout, elem_bytes, route=None):
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes,
            None if route is None else ("route", route.world, route.key), TRANSPOSE_VARIANT,
            BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB,
-           BAND_ROWS, BAND_DIAGS, TRANSPOSE_WARPS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE,
+           BAND_ROWS, BAND_DIAGS, BAND_WARPS, TRANSPOSE_WARPS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE,
            staging.BOX_BULK, staging.BOX_THREADS)
     plans = []
 
