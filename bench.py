@@ -181,31 +181,50 @@ def kernel_event_time(fn, iters):
 # CPU side (oracle port; test infrastructure, timed as the baseline only)
 # ---------------------------------------------------------------------------
 
+class CpuRemapSample:
+    """The C oracle port of the reference per-element remap, timed on this
+    host's cores over a bounded sample of the headline workload: buffers
+    built and the sample size calibrated once, then one timed sample per
+    step."""
+
+    def __init__(self):
+        import numpy as np
+        from oracle import oracle as O
+        self.O = O
+        # every host core (torchrun presets OMP_NUM_THREADS=1 for its workers)
+        O.set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+        self.spec = O.parse(HEADLINE_DSL)
+        self.n = N * N
+        self.src = (np.arange(self.n, dtype=np.uint32) & 0xFFFF).astype(np.uint16)
+        self.out = np.zeros(self.n, dtype=np.uint16)
+        self.count = N
+
+    def calibrate(self, target_seconds):
+        probe = 1 << 22
+        t0 = time.perf_counter()
+        self.O.remap(self.src, None, self.spec, first=0, count=probe, out=self.out)
+        dt = time.perf_counter() - t0
+        count = int(min(self.n, max(N, probe * target_seconds / max(dt, 1e-9))))
+        self.count = max(N, count - count % N)
+        return self.count
+
+    def run(self):
+        t0 = time.perf_counter()
+        self.O.remap(self.src, None, self.spec, first=0, count=self.count, out=self.out)
+        dt = time.perf_counter() - t0
+        gbs = 2 * 2 * self.count / dt / 1e9
+        threads = self.O.threads()
+        return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                "sample": f"{self.count} of {self.n} 16-bit elements ({self.count // N} rows; bf16 moved as "
+                          f"uint16 bit patterns) of the headline remap, oracle/lego_oracle.c per-element apply "
+                          f"(reference layout.py:313) with {threads} OpenMP threads, {dt:.2f} s"}
+
+
 def cpu_remap_rate(target_seconds=10.0):
-    """Time the C oracle port of the reference per-element remap on this
-    host's cores over a bounded sample of the headline workload."""
-    import numpy as np
-    from oracle import oracle as O
-    # every host core (torchrun presets OMP_NUM_THREADS=1 for its workers)
-    O.set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
-    spec = O.parse(HEADLINE_DSL)
-    n = N * N
-    src = (np.arange(n, dtype=np.int64) % 65536).astype(np.uint16)
-    out = np.zeros(n, dtype=np.uint16)
-    probe = 1 << 22
-    t0 = time.perf_counter()
-    O.remap(src, None, spec, first=0, count=probe, out=out)
-    dt = time.perf_counter() - t0
-    count = int(min(n, max(probe, probe * target_seconds / max(dt, 1e-9))))
-    count -= count % N
-    t0 = time.perf_counter()
-    O.remap(src, None, spec, first=0, count=count, out=out)
-    dt = time.perf_counter() - t0
-    gbs = 2 * 2 * count / dt / 1e9
-    return {"value": round(gbs, 3), "unit": "GB/s", "cores": O.threads(), "kind": "port",
-            "sample": f"{count} of {n} 16-bit elements ({count // N} rows; bf16 moved as uint16 bit patterns) of the headline remap, "
-                      f"oracle/lego_oracle.c per-element apply (reference layout.py:313) "
-                      f"with {O.threads()} OpenMP threads, {dt:.2f} s"}
+    """One calibrated sample of the CPU port (the GPU arm's cpu_baseline)."""
+    sample = CpuRemapSample()
+    sample.calibrate(target_seconds)
+    return sample.run()
 
 
 def run_reference(args):
@@ -213,10 +232,13 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # the whole run (W + K samples) targets about 90 s of CPU work
+    sample = CpuRemapSample()
+    sample.calibrate(max(0.05, 90.0 / max(1, args.warmup + args.steps)))
     rates = []
     base = None
     for k in range(args.warmup + args.steps):
-        r = cpu_remap_rate(target_seconds=max(1.0, 60.0 / max(1, args.warmup + args.steps)))
+        r = sample.run()
         if k >= args.warmup:
             rates.append(r["value"])
             base = r
