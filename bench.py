@@ -201,6 +201,7 @@ class CpuRemapSample:
 
     def calibrate(self, target_seconds):
         probe = 1 << 22
+        self.O.remap(self.src, None, self.spec, first=0, count=probe, out=self.out)   # threads, pages
         t0 = time.perf_counter()
         self.O.remap(self.src, None, self.spec, first=0, count=probe, out=self.out)
         dt = time.perf_counter() - t0
