@@ -581,7 +581,7 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
         const int half = (warp - 2) >> 2;
         constexpr int EPI_COLS = 256;                         // columns per epilogue warp
 #ifndef LEGO_GEMM_EPI_CHUNKS
-#define LEGO_GEMM_EPI_CHUNKS 2
+#define LEGO_GEMM_EPI_CHUNKS 4                              // measured: 4 chunks 681 us, 2 chunks 689 us (8192^3)
 #endif
         constexpr int EPI_CHUNKS = LEGO_GEMM_EPI_CHUNKS;      // 32-column TMEM loads in flight
         int it = 0;
