@@ -73,7 +73,7 @@ constexpr int MBAR_BYTES = NSLOT * 8;
 constexpr int CTRL_BYTES = 64;
 constexpr int SMEM_BYTES = RING_BYTES + BND_BYTES + MBAR_BYTES + CTRL_BYTES;
 #ifndef NW_POLL_NS
-#define NW_POLL_NS 0                                 // boundary poll back-off
+#define NW_POLL_NS 32                                // boundary poll back-off (measured: 32 ns 1068 us, 0 ns 1079 us)
 #endif
 
 #ifdef LEGO_NW_DEBUG
