@@ -626,7 +626,9 @@ def nw_score(sim, penalty: int, *, out=None, stream=None):
     return out
 
 
-GEMM_RASTER_GROUP = int(os.environ.get("LEGO_GEMM_GROUP", "16"))
+# measured (scripts/ab_gemm_group.py, 8192^3, 4 alternating runs each): G = 32 685 us,
+# 24 688, 48 688, 16 692, 64 695
+GEMM_RASTER_GROUP = int(os.environ.get("LEGO_GEMM_GROUP", "32"))
 
 
 def gemm(a, b, *, out=None, raster: Optional[int] = None, a_col: bool = False, b_col: bool = False,
