@@ -72,6 +72,12 @@ constexpr int BND_BYTES = BND_ROWS * 4;
 constexpr int MBAR_BYTES = NSLOT * 8;
 constexpr int CTRL_BYTES = 64;
 constexpr int SMEM_BYTES = RING_BYTES + BND_BYTES + MBAR_BYTES + CTRL_BYTES;
+#ifndef NW_PRODUCER_NS
+#define NW_PRODUCER_NS 64                            // producer back-off when nothing landed or was issued
+#endif
+#ifndef NW_FLUSHER_NS
+#define NW_FLUSHER_NS 64                             // flusher back-off while waiting for a computed block
+#endif
 #ifndef NW_POLL_NS
 #define NW_POLL_NS 32                                // boundary poll back-off (measured: 32 ns 1068 us, 0 ns 1079 us)
 #endif
@@ -414,7 +420,7 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
                         progress = true;
                     }
                 }
-                if (!progress) __nanosleep(64);
+                if (!progress) __nanosleep(NW_PRODUCER_NS);
             }
             gblk += total_blocks;
         } else if (warp == 2) {
@@ -468,7 +474,7 @@ nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, i
             for (int q = 0; q < CPL; ++q) ok[q] = col0 + 32 * q + lane < n;
             for (int k = 0; k < nblocks; ++k) {
                 NW_PROBE(5000000 + k);
-                while (ldv_acq(&ctrl->computed) < k) __nanosleep(64);
+                while (ldv_acq(&ctrl->computed) < k) __nanosleep(NW_FLUSHER_NS);
                 const int rows = min(BLK, n - k * BLK);
                 const int32_t* src = ring_gen + (k % NSLOT) * BLK * STRIP + lane;
                 int32_t* dst = sc + (long long)(k * BLK + 1) * ld + col0 + 1 + lane;
