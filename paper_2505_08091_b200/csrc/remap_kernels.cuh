@@ -98,43 +98,52 @@ static __device__ __forceinline__ T lego_map_one(long long x, int which) {
     else            gen::inv_fn(x, r);
     return (T)r;
 }
-// 4 consecutive indices per thread and one 16-byte (int32) / two 16-byte
-// (int64) stores when the output is 16-byte aligned; scalar tail
-template <typename T>
+// G consecutive indices per thread (G/4 16-byte int32 stores, or twice as
+// many for int64) when the output is 16-byte aligned; scalar tail.  The
+// memory-bound apply maps use G = 4 (fully coalesced stores); the
+// ALU-bound inverse maps G = 8 (more independent work per thread: +4 % on
+// the anti-diagonal inverse, where the half-coalesced stores cost nothing)
+template <typename T, int G>
 static __device__ __forceinline__ void lego_map_body(T* out, long long first, long long count,
                                                      int which) {
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
     long long done = 0;
     if ((reinterpret_cast<unsigned long long>(out) & 15) == 0) {
-        const long long nq = count >> 2;
+        const long long nq = count / G;
         for (long long q = tid; q < nq; q += stride) {
-            const long long x = first + 4 * q;
-            T v[4];
+            const long long x = first + G * q;
+            T v[G];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = lego_map_one<T>(x + u, which);
-            if (sizeof(T) == 4) {
-                *reinterpret_cast<int4*>(out + 4 * q) = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
-            } else {
-                *reinterpret_cast<longlong2*>(out + 4 * q) = make_longlong2((long long)v[0], (long long)v[1]);
-                *reinterpret_cast<longlong2*>(out + 4 * q + 2) = make_longlong2((long long)v[2], (long long)v[3]);
+            for (int u = 0; u < G; ++u) v[u] = lego_map_one<T>(x + u, which);
+#pragma unroll
+            for (int g = 0; g < G / 4; ++g) {
+                T* o = out + G * q + 4 * g;
+                if (sizeof(T) == 4) {
+                    *reinterpret_cast<int4*>(o) = make_int4((int)v[4 * g], (int)v[4 * g + 1], (int)v[4 * g + 2],
+                                                            (int)v[4 * g + 3]);
+                } else {
+                    *reinterpret_cast<longlong2*>(o) = make_longlong2((long long)v[4 * g], (long long)v[4 * g + 1]);
+                    *reinterpret_cast<longlong2*>(o + 2) = make_longlong2((long long)v[4 * g + 2],
+                                                                          (long long)v[4 * g + 3]);
+                }
             }
         }
-        done = nq << 2;
+        done = nq * G;
     }
     for (long long k = done + tid; k < count; k += stride) out[k] = lego_map_one<T>(first + k, which);
 }
 LEGO_GLOBAL void __launch_bounds__(256) lego_apply_map_i32(int* out, long long first, long long count) {
-    lego_map_body<int>(out, first, count, 0);
+    lego_map_body<int, 4>(out, first, count, 0);
 }
 LEGO_GLOBAL void __launch_bounds__(256) lego_apply_map_i64(long long* out, long long first, long long count) {
-    lego_map_body<long long>(out, first, count, 0);
+    lego_map_body<long long, 4>(out, first, count, 0);
 }
 LEGO_GLOBAL void __launch_bounds__(256) lego_inv_map_i32(int* out, long long first, long long count) {
-    lego_map_body<int>(out, first, count, 1);
+    lego_map_body<int, 8>(out, first, count, 1);
 }
 LEGO_GLOBAL void __launch_bounds__(256) lego_inv_map_i64(long long* out, long long first, long long count) {
-    lego_map_body<long long>(out, first, count, 1);
+    lego_map_body<long long, 8>(out, first, count, 1);
 }
 // histogram of apply over the whole logical space (bijectivity proof)
 LEGO_GLOBAL void __launch_bounds__(256) lego_hist(unsigned int* hist, long long count, long long n_out,
