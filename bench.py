@@ -324,7 +324,7 @@ def run(args):
             host_out[k].copy_(dev_out[k], non_blocking=True)
         main.wait_stream(s)
 
-    e2e_steps = max(4, args.steps // 8)
+    e2e_steps = max(8, args.steps // 4)
 
     def e2e_run():
         # the two streams overlap each other; main waits on both at the end
@@ -339,7 +339,7 @@ def run(args):
         for s in streams:
             main.wait_stream(s)
 
-    for _ in range(3):
+    for _ in range(6):
         e2e_step()
     torch.cuda.synchronize()
     barrier(world)
