@@ -55,12 +55,15 @@ typedef enum {
     LEGO_PROG_TRANSPOSE = 2,   /* remap: digit-permutation, register-tiled transpose   */
     LEGO_PROG_BAND = 3,        /* remap: anti-diagonal band tiles through shared memory */
     LEGO_PROG_SCATTER = 4,     /* remap into an injective layout: dst[apply(x)] = src[x] */
-    LEGO_PROG_STAGED = 5       /* remap: per-block source box staged through smem      */
+    LEGO_PROG_STAGED = 5,      /* remap: per-block source box staged through smem      */
+    LEGO_PROG_NW = 6           /* Needleman-Wunsch wavefront over a LEGO tile layout   */
 } lego_program_kind;
 
 /* Program geometry.  Index-map programs: n = logical size, units = physical
  * size.  Remap programs: n = destination elements per matrix (source
- * elements for SCATTER), units = CTAs per matrix (grid.x; grid.y = batch). */
+ * elements for SCATTER), units = CTAs per matrix (grid.x; grid.y = batch).
+ * NW programs: n = matrix side, units = tile rows H (= n for column strips),
+ * reserved = 1 when tiles publish bottom rows (more than one tile row). */
 
 typedef struct {
     int32_t kind;          /* lego_program_kind                                  */
@@ -137,13 +140,25 @@ lego_status lego_softmax_f32(const float *x, float *y, int64_t rows, int64_t col
  * sim is n x n; batch independent alignments back to back.
  * S[0][j] = -j*p, S[i][0] = -i*p,
  * S[i][j] = max(S[i-1][j-1] + sim[i-1][j-1], S[i-1][j] - p, S[i][j-1] - p).
- * Tiles are swept in anti-diagonal order with the LEGO antidiag layout.
+ * Column strips of 128 columns, each swept anti-diagonally by one CTA
+ * (the default layout of lego_nw_run, built into the library).
  * The kernel works on offset scores S + (i+j)p in int32: requires
  * |p| * (2n + 2) < 2^30 (else LEGO_E_ARG) and scores within +-2^30.
  * sim must be 16-byte aligned.  Stream-ordered; keeps a per-(device, stream)
  * scratch buffer of strips x n int32 between calls. */
 lego_status lego_nw_i32(const int32_t *sim, int32_t *score, int64_t n, int32_t penalty,
                         int64_t batch, void *stream);
+
+/* The same recurrence through a program generated from a LEGO layout of the
+ * cell grid (kernels.nw_layout / nw_program, LEGO_PROG_NW):
+ *   GroupBy([NR*H, NC*128]).OrderBy(RegP([NR,H,NC,128],[1,3,2,4])).OrderBy(T, I)
+ * T (over the NR x NC tile grid) is the order in which CTAs claim tiles, I
+ * (over a tile's H x 128 cells) the shared-memory order of its rows.  The
+ * host proves T a topological order of the tile dependencies and I
+ * row-preserving with 16-byte lane groups before building the program.
+ * n must equal the program's n; otherwise as lego_nw_i32. */
+lego_status lego_nw_run(lego_program p, const int32_t *sim, int32_t *score, int64_t n,
+                        int32_t penalty, int64_t batch, void *stream);
 
 /* bf16 GEMM on tcgen05/TMEM: C[b] = A[b] * B[b]^T-free layouts:
  * A is M x K row-major, B is N x K row-major ("TN"), C is M x N row-major

@@ -13,3 +13,18 @@ lego_status lego_cuda_check(cudaError_t e, const char* what);
         lego_status _s = (expr);            \
         if (_s != LEGO_OK) return _s;       \
     } while (0)
+
+// Needleman-Wunsch launch plan (wavefront.cu): validated sizes, tile grid and
+// the per-(device, stream) scratch, preset for one launch on `st`.
+struct NwPlan {
+    long long n, batch;
+    int H, nr, nc, total;     // tile rows, tile grid, tickets (batch * nr * nc)
+    int* ticket;              // claim counter (zeroed)
+    int* bnd;                 // right-column words per (matrix, tile column) (NW_EMPTY)
+    int* top;                 // tiled: bottom-row words per (matrix, tile) (NW_EMPTY), else null
+    unsigned ctas, border_ctas;
+    int smem;
+};
+lego_status lego_nw_prepare(const int32_t* sim, int32_t* score, int64_t n, int32_t penalty, int64_t batch,
+                            int64_t tile_rows, int tiled, cudaStream_t st, NwPlan* plan);
+int lego_nw_smem_bytes();   // dynamic shared memory of the wavefront kernel (nw_kernels.cuh)

@@ -194,6 +194,7 @@ struct lego_program_s {
     CUfunction_t remap = nullptr;
     CUfunction_t apply32 = nullptr, apply64 = nullptr, inv32 = nullptr, inv64 = nullptr;
     CUfunction_t hist = nullptr, hist_check = nullptr;
+    CUfunction_t nw_tiles = nullptr, nw_borders = nullptr;
 };
 
 extern "C" lego_status lego_program_load(const void* cubin, size_t cubin_len,
@@ -223,6 +224,26 @@ extern "C" lego_status lego_program_load(const void* cubin, size_t cubin_len,
             g_drv.unload(p->mod);
             delete p;
             return lego_fail(LEGO_E_ARG, "index-map program lacks its kernels");
+        }
+    } else if (info->kind == LEGO_PROG_NW) {
+        if (info->smem_bytes != lego_nw_smem_bytes()) {
+            g_drv.unload(p->mod);
+            delete p;
+            return lego_fail(LEGO_E_ARG, "NW program shared memory %d != the library's %d", info->smem_bytes,
+                             lego_nw_smem_bytes());
+        }
+        bool ok = !g_drv.get_fn(&p->nw_tiles, p->mod, "lego_nw_tiles") &&
+                  !g_drv.get_fn(&p->nw_borders, p->mod, "lego_nw_borders");
+        if (!ok) {
+            g_drv.unload(p->mod);
+            delete p;
+            return lego_fail(LEGO_E_ARG, "NW program lacks its kernels");
+        }
+        if ((s = drv_check(g_drv.set_attr(p->nw_tiles, 8 /*MAX_DYNAMIC_SHARED_SIZE_BYTES*/, info->smem_bytes),
+                           "cuFuncSetAttribute(nw)"))) {
+            g_drv.unload(p->mod);
+            delete p;
+            return s;
         }
     } else {
         if ((s = drv_check(g_drv.get_fn(&p->remap, p->mod, "lego_remap"), "cuModuleGetFunction(lego_remap)"))) {
@@ -310,6 +331,26 @@ extern "C" lego_status lego_check_bijective(lego_program p, uint32_t* hist, int6
     if ((s = lego_cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return s;
     *violations = (int64_t)host;
     return LEGO_OK;
+}
+
+extern "C" lego_status lego_nw_run(lego_program p, const int32_t* sim, int32_t* score, int64_t n,
+                                   int32_t penalty, int64_t batch, void* stream) {
+    if (!p || p->info.kind != LEGO_PROG_NW) return lego_fail(LEGO_E_ARG, "program is not an NW program");
+    if (n != p->info.n)
+        return lego_fail(LEGO_E_SHAPE, "program was built for n = %lld, called with n = %lld",
+                         (long long)p->info.n, (long long)n);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    NwPlan pl;
+    lego_status s = lego_nw_prepare(sim, score, n, penalty, batch, p->info.units, p->info.reserved & 1, st, &pl);
+    if (s || batch == 0) return s;
+    long long nn = n, bb = batch;
+    int pp = penalty;
+    void* a1[] = {&score, &nn, &pp, &bb};
+    if ((s = launch(p->nw_borders, pl.border_ctas, 1, 256, 0, stream, a1))) return s;
+    if (n == 0) return LEGO_OK;
+    int ni = (int)n;
+    void* a2[] = {&sim, &score, &ni, &pp, &pl.H, &pl.nr, &pl.nc, &pl.total, &pl.ticket, &pl.bnd, &pl.top};
+    return launch(p->nw_tiles, pl.ctas, 1, 128, (unsigned)pl.smem, stream, a2);
 }
 
 extern "C" lego_status lego_remap(lego_program p, const void* src, void* dst, int64_t batch,

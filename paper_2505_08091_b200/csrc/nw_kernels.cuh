@@ -1,0 +1,677 @@
+// nw_kernels.cuh -- Needleman-Wunsch score matrix as a wavefront over LEGO
+// tiles (BASELINE.json config 4b).  Kernel template shared by the static
+// library kernel (wavefront.cu: column strips, row-major ring) and the
+// programs generated from a user layout (kernels.nw_program: NVRTC, with a
+// `namespace gen` of LEGO index functions in front of this file).
+//
+//   S[0][j] = -j*p,  S[i][0] = -i*p,
+//   S[i][j] = max(S[i-1][j-1] + sim[i-1][j-1], S[i-1][j] - p, S[i][j-1] - p)
+//
+// Offset scores.  With S'[i][j] = S[i][j] + (i+j)*p the recurrence becomes
+//   S'[i][j] = max(S'[i-1][j-1] + sim[i-1][j-1] + 2p, S'[i-1][j], S'[i][j-1])
+// with all-zero borders: the left-to-right dependency chain is one integer
+// max per cell (no subtract), and the conversion back to S happens in the
+// store path, off the chain.  Exact whenever |p|*(2n+2) < 2^30 and the true
+// scores fit in +-2^30 (checked on p; sim is the caller's contract).
+//
+// The layout (kernels.nw_layout; reference GroupBy/OrderBy semantics,
+// pkg/src/lego/layout.py:206-334) over the cells of the padded n x n grid is
+//   GroupBy([NR*H, NC*128]).OrderBy(RegP([NR,H,NC,128],[1,3,2,4])).OrderBy(T, I)
+// i.e. position = T(a, b) * (H*128) + I(r, c) for cell (a*H + r, b*128 + c):
+//  * T, the tile order, is the order in which CTAs claim tiles from an atomic
+//    ticket: ticket t -> tile T^-1(t), generated as gen::tile_of.  The host
+//    proves T is a topological order of the tile dependency graph (every
+//    tile after its upper and left neighbours), so a persistent grid that
+//    claims in ticket order never waits on an unclaimed tile;
+//  * I, the cell order inside a tile, is the shared-memory order of the
+//    tile's rows in the staging ring (the paper's LEGO-permuted NW buffer,
+//    PAPER.md:1298-1301).  It must keep each row in its ring row and each
+//    lane's 4-column group contiguous (one 16-byte vector); gen::slot(r, g)
+//    gives the 16-byte slot of group g in tile row r.  The host proves both.
+//
+// Inside a tile (no host loop over diagonals, no grid sync), four warp roles
+// per CTA, one per SM sub-partition:
+//   warp 0  compute:  sweeps the tile anti-diagonally over 4x4 cell blocks --
+//           lane j owns columns 4j..4j+3 and at step s computes rows
+//           4(s-j) .. 4(s-j)+3, i.e. each step is one anti-diagonal of the
+//           (row quads x 32 lane-columns) grid.  The four left values arrive
+//           by one warp shuffle each; everything else is in registers or
+//           16-byte shared loads prefetched two steps ahead;
+//   warp 1  producer: cp.async-stages sim, 32 rows x 128 columns per block,
+//           into a 12-block ring (the compute warp overwrites each sim row
+//           with its S' row in place);
+//   warp 2  boundary: polls the left tile's published last column (32-bit
+//           words in global memory, preset to a sentinel no offset score can
+//           take) and hands it in row order, through a shared ring and a row
+//           counter, to compute lane 0; in tiled mode it first fetches the
+//           upper tile's published bottom row the same way;
+//   warp 3  flusher:  converts finished blocks S' -> S and writes them out
+//           as coalesced row segments.
+// Roles synchronise through monotonic block counters in shared memory
+// (loaded / computed / flushed); the compute warp checks them once per 32
+// rows with a prefetched load, so its step body has no barrier.
+//
+// Includer-provided switches:
+//   NW_TILED      0: one tile per column strip (H = n, no top rows);
+//                 1: tiles of H rows publish their bottom row for the tile below
+//   NW_GEN_TILES  1: gen::tile_of(t, x) gives the row-major tile index x of ticket t
+//   NW_GEN_SLOTS  1: gen::slot(r, g, s) gives the ring slot of lane group g in row r
+#pragma once
+
+#ifndef NW_TILED
+#define NW_TILED 0
+#endif
+#ifndef NW_GEN_TILES
+#define NW_GEN_TILES 0
+#endif
+#ifndef NW_GEN_SLOTS
+#define NW_GEN_SLOTS 0
+#endif
+#ifndef NW_GLOBAL
+#define NW_GLOBAL extern "C" __global__
+#endif
+
+namespace nwk {
+
+typedef unsigned int u32;
+
+constexpr int CPL = 4;                               // columns per lane
+constexpr int STRIP = 32 * CPL;                      // columns per tile
+constexpr int BLK = 32;                              // rows per block
+#ifndef NW_RPS
+#define NW_RPS 4                                     // rows per lane per step
+#endif
+constexpr int RPS = NW_RPS;
+constexpr int STEPS = BLK / RPS;                     // compute steps per block
+constexpr int BLAG = (31 + STEPS - 1) / STEPS + 1;   // lane 31 completes block k before block k+BLAG starts
+constexpr int DRAIN = (31 + STEPS - 1) / STEPS;      // extra blocks cover lane 31's 31-step lag
+#ifndef NW_GRP
+#define NW_GRP (16 / NW_RPS)                         // measured: 4 steps 1068 us, 2 steps 1075, 1 step 1126 (n = 16384)
+#endif
+constexpr int GRP = NW_GRP;                          // boundary readiness checked every GRP steps
+constexpr int NSLOT = 12;                            // ring blocks
+constexpr int RING_ROWS = NSLOT * BLK;               // 384
+constexpr int BND_ROWS = 256;                        // boundary ring (rows)
+constexpr int BND_GROUPS = BND_ROWS / BLK;
+constexpr int ROW_BYTES = STRIP * 4;                 // 512
+constexpr int RING_BYTES = RING_ROWS * ROW_BYTES;    // 192 KiB
+constexpr int BND_BYTES = BND_ROWS * 4;
+constexpr int MBAR_BYTES = NSLOT * 8;
+constexpr int CTRL_BYTES = 64;
+constexpr int TOP_BYTES = (STRIP + 4) * 4;           // upper tile's bottom row + the corner
+constexpr int SMEM_BYTES = RING_BYTES + BND_BYTES + MBAR_BYTES + CTRL_BYTES + TOP_BYTES;
+#ifndef NW_PRODUCER_NS
+#define NW_PRODUCER_NS 64                            // producer back-off when nothing landed or was issued
+#endif
+#ifndef NW_FLUSHER_NS
+#define NW_FLUSHER_NS 64                             // flusher back-off while waiting for a computed block
+#endif
+#ifndef NW_POLL_NS
+#define NW_POLL_NS 32                                // boundary poll back-off (measured: 32 ns 1068 us, 0 ns 1079 us)
+#endif
+
+// boundary words start as NW_EMPTY (|S'| < 2^30 never equals it)
+constexpr int NW_EMPTY = (int)0x80808080;
+
+#ifdef LEGO_NW_DEBUG
+// event times (globaltimer ns, low 32 bits): g_nw_trace[(cta * 4 + role) * 2048 + idx]
+__device__ unsigned g_nw_trace[148 * 4 * 2048];
+__device__ __forceinline__ unsigned nw_now() {
+    unsigned t;
+    asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(t));
+    return t;
+}
+#define NW_TRACE(role, idx) \
+    do { if ((idx) < 2048) nwk::g_nw_trace[(blockIdx.x * 4 + (role)) * 2048 + (idx)] = nwk::nw_now(); } while (0)
+#else
+#define NW_TRACE(role, idx) ((void)0)
+#endif
+
+struct Ctrl {
+    int tile;        // claimed ticket
+    int loaded;      // sim blocks <= loaded have landed
+    int computed;    // S' blocks <= computed are final
+    int flushed;     // blocks <= flushed are written out (ring slot reusable)
+    int ready;       // boundary rows < ready are in the shared ring
+    int top;         // tiled mode: the upper tile's bottom row is in shared memory
+};
+
+// role counters in shared memory.  Publication is a release store at CTA
+// scope (the guarded data was written before it, after a __syncwarp); the
+// helper warps read counters with acquire loads.  The compute warp's hot
+// loop polls `ready` / `loaded` with plain volatile loads: an acquire there
+// costs 4 % of the kernel (1121 vs 1075 us at n = 16384), and the shared-
+// memory accesses of one SM's warps are performed in issue order by its one
+// shared-memory pipeline, which is what the pattern relies on.
+__device__ __forceinline__ int ldv(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ int ldv_acq(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v)
+                 : "r"((u32)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void stv(int* p, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" :: "r"((u32)__cvta_generic_to_shared(p)), "r"(v)
+                 : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(u32 dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(u32 dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ int ld_bnd(const int* p) {
+    int w;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(w) : "l"(p) : "memory");
+    return w;
+}
+__device__ __forceinline__ int4 ld_bnd4(const int* p) {
+    int4 w;
+    asm volatile("ld.relaxed.gpu.global.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "l"(p) : "memory");
+    return w;
+}
+
+// ---------------------------------------------------------------------------
+// LEGO maps: tile order and ring slots
+// ---------------------------------------------------------------------------
+// tile of ticket t (tiles row-major over NR x NC)
+__device__ __forceinline__ void tile_of(long long t, int nc, int& a, int& b) {
+#if NW_GEN_TILES
+    long long x;
+    gen::tile_of(t, x);
+    a = (int)(x / nc);
+    b = (int)(x - (long long)a * nc);
+#else
+    a = (int)(t / nc);
+    b = (int)(t - (long long)a * nc);
+#endif
+}
+// 16-byte slot of lane group g (columns 4g..4g+3) in tile row r
+__device__ __forceinline__ int slot(int r, int g, int h) {
+#if NW_GEN_SLOTS
+    long long s;
+    gen::slot((long long)min(max(r, 0), h - 1), (long long)g, s);
+    return (int)s;
+#else
+    (void)r;
+    (void)h;
+    return g;
+#endif
+}
+
+// compute-warp state: S' of the lane's 4 columns in its last finished row,
+// the diagonal predecessor of its first column, the last-column values it
+// sends right, and sim rows prefetched two steps ahead
+struct Lane {
+    int h[CPL];
+    int dprev;
+    int send[RPS];
+    int4 nx1[RPS], nx2[RPS];
+    int bv[RPS];
+};
+
+template <int N>
+__device__ __forceinline__ void ldsv(u32 a, int (&v)[N]);
+template <>
+__device__ __forceinline__ void ldsv<2>(u32 a, int (&v)[2]) {
+    asm volatile("ld.volatile.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(a));
+}
+template <>
+__device__ __forceinline__ void ldsv<4>(u32 a, int (&v)[4]) {
+    asm volatile("ld.volatile.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(a));
+}
+
+// predicated (branch-free) publication of RPS consecutive boundary words
+__device__ __forceinline__ void publish(int* p, int pred, const int (&v)[RPS]) {
+#if NW_RPS == 4
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\t"
+        "@q st.relaxed.gpu.global.v4.b32 [%0], {%2, %3, %4, %5};\n\t}"
+        :: "l"(p), "r"(pred), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]) : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\t"
+        "@q st.relaxed.gpu.global.v2.b32 [%0], {%2, %3};\n\t}"
+        :: "l"(p), "r"(pred), "r"(v[0]), "r"(v[1]) : "memory");
+#endif
+}
+__device__ __forceinline__ void publish4(int* p, int pred, int x0, int x1, int x2, int x3) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\t"
+        "@q st.relaxed.gpu.global.v4.b32 [%0], {%2, %3, %4, %5};\n\t}"
+        :: "l"(p), "r"(pred), "r"(x0), "r"(x1), "r"(x2), "r"(x3) : "memory");
+}
+
+__device__ __forceinline__ int ring_wrap(int r) { return r >= RING_ROWS ? r - RING_ROWS : r; }
+__device__ __forceinline__ int ring_mod(int r) {
+    int m = r % RING_ROWS;
+    return m < 0 ? m + RING_ROWS : m;
+}
+// the int4 cell of lane group `lane` in ring row rm (tile row r)
+__device__ __forceinline__ int4* ring_cell(int4* ring4, int rm, int r, int lane, int h) {
+    return ring4 + (rm << 5) + slot(r, lane, h);
+}
+
+// Tile geometry shared by the roles.
+struct Tile {
+    int bm;          // matrix of the batch
+    int a, b;        // tile row / column
+    int row0, col0;  // first interior row / column
+    int rows;        // interior rows in this tile
+    int nblocks;     // 32-row blocks
+    int* my_bnd;     // this tile column's right-column words, indexed by interior row
+    int* top_in;     // tiled: the bottom row of the tile above (128 words), or null
+    int* top_out;    // tiled: where this tile publishes its bottom row, or null
+};
+
+// one anti-diagonal step of the compute warp: lane j computes the RPS x 4
+// block rows r0 = RPS(s-j) .. r0+RPS-1 (tile rows), columns 4j..4j+3 of the tile
+// rm = r0 mod RING_ROWS (RPS | RING_ROWS, so rows r0 .. r0+RPS-1 never straddle the wrap)
+template <bool GUARD>
+__device__ __forceinline__ void nw_step(Lane& c, int s, int lane, int4* ring4, u32 bnd, int p2, const Tile& tl,
+                                        int h, int* pub_row, int rm) {
+    const int r0 = RPS * (s - lane);
+    const int rmp = ring_wrap(rm + 2 * RPS);
+    int4 cur[RPS];
+    int lb[RPS];
+#pragma unroll
+    for (int q = 0; q < RPS; ++q) {
+        cur[q] = c.nx1[q];
+        c.nx1[q] = c.nx2[q];
+#ifndef NW_ABL_NOLDS
+        c.nx2[q] = *ring_cell(ring4, rmp + q, r0 + 2 * RPS + q, lane, h);
+#else
+        c.nx2[q] = make_int4(q, lane, s, q ^ lane);
+#endif
+        lb[q] = c.bv[q];
+    }
+    ldsv<RPS>(bnd + (u32)(((RPS * (s + 1)) & (BND_ROWS - 1)) * 4), c.bv);   // next step's boundary
+    int left[RPS];
+#pragma unroll
+    for (int q = 0; q < RPS; ++q) {
+#ifndef NW_ABL_NOSHFL
+        const int sl = __shfl_up_sync(0xffffffffu, c.send[q], 1);
+#else
+        const int sl = c.send[q] + q;                   // ablation: no lane exchange (wrong results)
+#endif
+        left[q] = lane == 0 ? lb[q] : sl;
+    }
+    const bool live = !GUARD || r0 >= 0;                // lanes start one step apart
+    int up0 = c.h[0], up1 = c.h[1], up2 = c.h[2], up3 = c.h[3];
+    int d = c.dprev;
+#pragma unroll
+    for (int q = 0; q < RPS; ++q) {
+        const int x0 = max(max(cur[q].x + d + p2, up0), left[q]);
+        const int x1 = max(max(cur[q].y + up0 + p2, up1), x0);
+        const int x2 = max(max(cur[q].z + up1 + p2, up2), x1);
+        const int x3 = max(max(cur[q].w + up2 + p2, up3), x2);
+#ifndef NW_ABL_NOSTS
+        if (live) *ring_cell(ring4, rm + q, r0 + q, lane, h) = make_int4(x0, x1, x2, x3);   // S' replaces sim in place
+#endif
+        up0 = x0; up1 = x1; up2 = x2; up3 = x3;
+        d = left[q];
+        c.send[q] = live ? x3 : c.send[q];
+    }
+    c.h[0] = live ? up0 : c.h[0];
+    c.h[1] = live ? up1 : c.h[1];
+    c.h[2] = live ? up2 : c.h[2];
+    c.h[3] = live ? up3 : c.h[3];
+    c.dprev = live ? d : c.dprev;
+    // the tile's last column goes to the right neighbour (lane 31, rows of the tile)
+    const int pub = (lane == 31) & (r0 < tl.rows) & live;
+#ifndef NW_ABL_NOPUB
+    publish(pub_row, pub, c.send);
+#endif
+#if NW_TILED
+    // the tile's last row goes to the tile below (every lane, its 4 columns)
+    publish4(tl.top_out + 4 * lane, (tl.top_out != nullptr) & (r0 + RPS == tl.rows), up0, up1, up2, up3);
+#endif
+}
+
+// one block of STEPS steps (32 rows of lane 0); boundary readiness is checked
+// every GRP steps against a counter value prefetched GRP steps earlier
+template <bool GUARD>
+__device__ __forceinline__ void nw_block(Lane& c, int k, int lane, int4* ring4, u32 bnd, int p2, const Tile& tl,
+                                         int h, int& rd, const int* ready, int rows_total) {
+    int* pub_blk = tl.my_bnd + tl.row0 + RPS * (k * STEPS - lane);  // lane 31's rows of step u: + RPS*u
+    int rm = ring_mod(k * BLK - RPS * lane);
+#pragma unroll
+    for (int u = 0; u < STEPS; ++u) {
+        const int s = k * STEPS + u;
+        if (u % GRP == 0) {                             // rows used (and prefetched) through step s + GRP
+            const int need = min(RPS * (s + GRP + 1), rows_total);   // the helper stops at rows_total
+            while (rd < need) rd = ldv(ready);
+            rd = ldv(ready);
+        }
+        nw_step<GUARD>(c, s, lane, ring4, bnd, p2, tl, h, pub_blk + RPS * u, rm);
+        rm = ring_wrap(rm + RPS);
+    }
+}
+
+// Kernel body.  Tiles: NR x NC per matrix, H rows x 128 columns each
+// (NR = 1, H = n in strip mode); total = batch * NR * NC tickets.
+// bnd_g: per (matrix, tile column) n_pad words (the column's right edge,
+// by interior row); top_g (tiled): per (matrix, tile) 128 words (the bottom
+// row of the tile above it).  Both preset to NW_EMPTY by the launcher.
+__device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* __restrict__ score, int n, int p,
+                                              int H, int nr, int nc, int total, int* __restrict__ ticket,
+                                              int* __restrict__ bnd_g, int* __restrict__ top_g) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    int* ring_gen = reinterpret_cast<int*>(smem);
+    Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem + RING_BYTES + BND_BYTES + MBAR_BYTES);
+    int* top_s = reinterpret_cast<int*>(smem + RING_BYTES + BND_BYTES + MBAR_BYTES + CTRL_BYTES);
+    const u32 ring = static_cast<u32>(__cvta_generic_to_shared(smem));
+    const u32 bnd = ring + RING_BYTES;
+    const u32 mbar = bnd + BND_BYTES;
+    int gblk = 0;                                    // producer: blocks issued in earlier tiles
+    if (threadIdx.x < NSLOT)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" :: "r"(mbar + 8u * threadIdx.x) : "memory");
+    const int lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);   // warp-uniform role
+    const int n_pad = (n + BLK - 1) / BLK * BLK;
+    const int tiles_per_matrix = nr * nc;
+
+    for (;;) {
+        if (threadIdx.x == 0) {
+            ctrl->tile = atomicAdd(ticket, 1);
+            ctrl->loaded = ctrl->computed = ctrl->flushed = -1;
+            ctrl->ready = 0;
+            ctrl->top = 0;
+        }
+        __syncthreads();
+        const int t = ctrl->tile;
+        if (t >= total) return;
+        Tile tl;
+        tl.bm = t / tiles_per_matrix;
+        tile_of(t - tl.bm * tiles_per_matrix, nc, tl.a, tl.b);
+        tl.row0 = tl.a * H;
+        tl.col0 = tl.b * STRIP;
+        tl.rows = min(H, n - tl.row0);
+        tl.nblocks = (tl.rows + BLK - 1) / BLK;
+        tl.my_bnd = bnd_g + (long long)(tl.bm * nc + tl.b) * n_pad;
+#if NW_TILED
+        {
+            const long long tid = (long long)tl.bm * tiles_per_matrix + (long long)tl.a * nc + tl.b;
+            tl.top_in = tl.a > 0 ? top_g + tid * STRIP : nullptr;
+            tl.top_out = tl.a + 1 < nr ? top_g + (tid + nc) * STRIP : nullptr;
+        }
+#else
+        tl.top_in = tl.top_out = nullptr;
+#endif
+        const int rows_total = (tl.nblocks + DRAIN) * BLK;
+
+        if (warp == 0) {
+            // ---------------- compute ----------------
+            Lane c;
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) c.h[q] = 0;
+#pragma unroll
+            for (int q = 0; q < RPS; ++q) c.send[q] = 0;
+            c.dprev = 0;
+#if NW_TILED
+            if (tl.top_in) {                            // S' of the row above the tile
+                while (ldv_acq(&ctrl->top) == 0) {}
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) c.h[q] = top_s[CPL * lane + q];
+                c.dprev = lane == 0 ? top_s[STRIP] : top_s[CPL * lane - 1];
+            }
+#endif
+            const int p2 = 2 * p;
+            int4* ring4 = reinterpret_cast<int4*>(smem);
+            int pl = ldv(&ctrl->loaded);
+            int rd = ldv(&ctrl->ready);
+            for (int k = 0; k < tl.nblocks + DRAIN; ++k) {
+                if (lane == 0) NW_TRACE(0, k);
+                if (k >= BLAG) {                        // lane 31 has finished block k - BLAG
+                    __syncwarp();
+                    if (lane == 0) stv(&ctrl->computed, k - BLAG);
+                }
+                // the last steps of block k prefetch block k+1's first rows: need both
+                const int need_blk = min(k + 1, tl.nblocks + DRAIN - 1);
+                while (pl < need_blk) pl = ldv(&ctrl->loaded);
+                if (k == 0) {                           // operands of the first two steps
+                    while (rd < RPS) rd = ldv(&ctrl->ready);
+#pragma unroll
+                    for (int q = 0; q < RPS; ++q) {
+                        c.nx1[q] = *ring_cell(ring4, ring_mod(-RPS * lane + q), -RPS * lane + q, lane, H);
+                        c.nx2[q] = *ring_cell(ring4, ring_mod(RPS - RPS * lane + q), RPS - RPS * lane + q, lane, H);
+                    }
+                    ldsv<RPS>(bnd, c.bv);
+                }
+                pl = ldv(&ctrl->loaded);                // prefetch for the next block
+                if (k < (31 + STEPS - 1) / STEPS)
+                    nw_block<true>(c, k, lane, ring4, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
+                else
+                    nw_block<false>(c, k, lane, ring4, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
+            }
+            __syncwarp();
+            if (lane == 0) stv(&ctrl->computed, tl.nblocks + DRAIN - 1);
+        } else if (warp == 1) {
+            // ---------------- producer: sim blocks -> ring ----------------
+            // Issues block k once its ring slot is flushed; each block's
+            // copies arrive on a per-slot mbarrier, polled without blocking so
+            // `loaded` is published as soon as a block lands.
+            const int* simb = sim + (long long)tl.bm * n * n + (long long)tl.row0 * n;
+            const bool vec = (n & 3) == 0;
+            const int total_blocks = tl.nblocks + DRAIN;
+            int issued = 0, landed = 0;
+            while (landed < total_blocks) {
+                bool progress = false;
+                if (issued < total_blocks && (issued < NSLOT || ldv_acq(&ctrl->flushed) >= issued - NSLOT)) {
+                    const int k = issued;
+                    const u32 mb = mbar + 8u * (u32)((gblk + k) % NSLOT);
+                    if (k < tl.nblocks) {
+                        const int rows = min(BLK, tl.rows - k * BLK);
+                        const u32 blk = ring + (u32)((k % NSLOT) * BLK * ROW_BYTES);
+                        if (vec) {
+                            const bool ok = tl.col0 + CPL * lane < n;
+                            const int* src = simb + (long long)k * BLK * n + tl.col0 + CPL * lane;
+#pragma unroll 8
+                            for (int r = 0; r < rows; ++r) {
+                                if (ok) cp_async16(blk + (u32)(r * ROW_BYTES + 16 * slot(k * BLK + r, lane, H)), src);
+                                src += n;
+                            }
+                        } else {
+                            const int* src = simb + (long long)k * BLK * n + tl.col0 + lane;
+                            for (int r = 0; r < rows; ++r) {
+#pragma unroll
+                                for (int q = 0; q < CPL; ++q) {
+                                    const int col = 32 * q + lane;
+                                    if (tl.col0 + col < n)
+                                        cp_async4(blk + (u32)(r * ROW_BYTES + 16 * slot(k * BLK + r, col >> 2, H)
+                                                              + 4 * (col & 3)), src + 32 * q);
+                                }
+                                src += n;
+                            }
+                        }
+                        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(mb) : "memory");
+                    } else {
+                        asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}"
+                                     :: "r"(mb) : "memory");
+                    }
+                    ++issued;
+                    progress = true;
+                }
+                if (landed < issued) {
+                    const int g = gblk + landed;
+                    u32 ok;
+                    asm volatile("{\n\t.reg .pred p;\n\t"
+                                 "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                                 "selp.u32 %0, 1, 0, p;\n\t}"
+                                 : "=r"(ok) : "r"(mbar + 8u * (u32)(g % NSLOT)), "r"((g / NSLOT) & 1)
+                                 : "memory");
+                    if (__all_sync(0xffffffffu, ok)) {
+                        if (lane == 0) {
+                            stv(&ctrl->loaded, landed);
+                            NW_TRACE(1, landed);
+                        }
+                        ++landed;
+                        progress = true;
+                    }
+                }
+                if (!progress) __nanosleep(NW_PRODUCER_NS);
+            }
+            gblk += total_blocks;
+        } else if (warp == 2) {
+            // ---------------- boundary: neighbours' edges -> shared memory ----------------
+#if NW_TILED
+            if (tl.top_in) {
+                // the upper tile's bottom row (lane l: columns 4l..4l+3) and the
+                // corner S'[row0-1][col0-1] (the left column's word, or the border)
+                int4 v = ld_bnd4(tl.top_in + CPL * lane);
+                while (v.x == NW_EMPTY || v.y == NW_EMPTY || v.z == NW_EMPTY || v.w == NW_EMPTY) {
+                    __nanosleep(NW_POLL_NS);
+                    v = ld_bnd4(tl.top_in + CPL * lane);
+                }
+                top_s[CPL * lane + 0] = v.x;
+                top_s[CPL * lane + 1] = v.y;
+                top_s[CPL * lane + 2] = v.z;
+                top_s[CPL * lane + 3] = v.w;
+                if (lane == 0) {
+                    int corner = 0;
+                    if (tl.b > 0) {
+                        const int* cp = tl.my_bnd - n_pad + tl.row0 - 1;
+                        corner = ld_bnd(cp);
+                        while (corner == NW_EMPTY) {
+                            __nanosleep(NW_POLL_NS);
+                            corner = ld_bnd(cp);
+                        }
+                    }
+                    top_s[STRIP] = corner;
+                }
+                __syncwarp();
+                if (lane == 0) stv(&ctrl->top, 1);
+            }
+#endif
+            // Lane l polls row 32m + l of the left column; rows are handed to
+            // the compute warp in order through ctrl->ready as soon as a
+            // prefix of the group is in.
+            const int* left = tl.my_bnd - n_pad + tl.row0;
+            const int groups = tl.nblocks + DRAIN;
+            for (int m = 0; m < groups; ++m) {
+                const int r = m * BLK + lane;
+                if (m >= BND_GROUPS) {
+                    while (ldv_acq(&ctrl->computed) < m - BND_GROUPS) __nanosleep(128);
+                }
+                int v = 0;                              // S'[r+1][0] = 0 on the matrix edge
+                bool ok = true;
+                if (tl.b > 0 && r < tl.rows) {
+                    v = ld_bnd(left + r);
+                    ok = v != NW_EMPTY;
+                }
+                bool written = false;
+                int told = 0;
+                for (;;) {
+                    const unsigned ball = __ballot_sync(0xffffffffu, ok);
+                    const int tt = ball == 0xffffffffu ? 32 : __ffs(~ball) - 1;   // ready prefix
+                    if (ok && !written && lane < tt) {
+                        asm volatile("st.shared.b32 [%0], %1;" :: "r"(bnd + (u32)((r & (BND_ROWS - 1)) * 4)),
+                                     "r"(v) : "memory");
+                        written = true;
+                    }
+                    if (tt > told) {
+                        __syncwarp();
+                        if (lane == 0) stv(&ctrl->ready, m * BLK + tt);
+                        told = tt;
+                    }
+                    if (tt == 32) break;
+                    if (NW_POLL_NS) __nanosleep(NW_POLL_NS);
+                    if (!ok) {
+                        v = ld_bnd(left + r);
+                        ok = v != NW_EMPTY;
+                    }
+                }
+                if (lane == 31) NW_TRACE(2, m);
+            }
+        } else {
+            // ---------------- flusher: S' -> S, coalesced row segments ----------------
+            int* sc = score + (long long)tl.bm * ((long long)n + 1) * ((long long)n + 1);
+            const long long ld = (long long)n + 1;
+            bool ok[CPL];
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) ok[q] = tl.col0 + 32 * q + lane < n;
+            for (int k = 0; k < tl.nblocks; ++k) {
+                while (ldv_acq(&ctrl->computed) < k) __nanosleep(NW_FLUSHER_NS);
+                const int rows = min(BLK, tl.rows - k * BLK);
+                const int* src = ring_gen + (k % NSLOT) * BLK * STRIP;
+                int* dst = sc + (long long)(tl.row0 + k * BLK + 1) * ld + tl.col0 + 1 + lane;
+                int off = (tl.row0 + k * BLK + tl.col0 + lane + 2) * p;   // (i + j) * p of column lane, row k*BLK
+#if NW_GEN_SLOTS
+                // cell (r, 32q + lane) sits at slot(r, (32q + lane) / 4) * 4 + lane % 4 of its ring row
+#pragma unroll 2
+                for (int r = 0; r < rows; ++r) {
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q)
+                        if (ok[q])
+                            dst[32 * q] = src[r * STRIP + 4 * slot(k * BLK + r, 8 * q + (lane >> 2), H) + (lane & 3)]
+                                          - (off + 32 * q * p);
+                    dst += ld;
+                    off += p;
+                }
+#else
+                if (rows == BLK && tl.col0 + STRIP <= n) {
+                    // full block: 16 rows of loads in flight before their stores
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        int v[16][CPL];
+#pragma unroll
+                        for (int r = 0; r < 16; ++r)
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) v[r][q] = src[(16 * hh + r) * STRIP + 32 * q + lane];
+#pragma unroll
+                        for (int r = 0; r < 16; ++r) {
+                            int* d = dst + (16 * hh + r) * ld;
+                            const int o = off + (16 * hh + r) * p;
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) d[32 * q] = v[r][q] - (o + 32 * q * p);
+                        }
+                    }
+                } else {
+                    src += lane;
+#pragma unroll 4
+                    for (int r = 0; r < rows; ++r) {
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q)
+                            if (ok[q]) dst[32 * q] = src[32 * q] - (off + 32 * q * p);
+                        dst += ld;
+                        src += STRIP;
+                        off += p;
+                    }
+                }
+#endif
+                __syncwarp();
+                if (lane == 0) { stv(&ctrl->flushed, k); NW_TRACE(3, k); }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void nw_borders_body(int* __restrict__ score, long long n, int p, long long batch) {
+    const long long w = n + 1;
+    const long long total = batch * w;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+         k += (long long)gridDim.x * blockDim.x) {
+        const long long b = k / w, x = k - b * w;
+        int* s = score + b * w * w;
+        s[x] = (int)(-x * p);          // row 0
+        s[x * w] = (int)(-x * p);      // column 0
+    }
+}
+
+}  // namespace nwk
+
+// launch entry points (extern "C" in generated programs: cuModuleGetFunction names)
+NW_GLOBAL void __launch_bounds__(128, 1)
+lego_nw_tiles(const int* __restrict__ sim, int* __restrict__ score, int n, int p, int H, int nr, int nc, int total,
+              int* __restrict__ ticket, int* __restrict__ bnd_g, int* __restrict__ top_g) {
+    nwk::nw_tiles_body(sim, score, n, p, H, nr, nc, total, ticket, bnd_g, top_g);
+}
+
+NW_GLOBAL void lego_nw_borders(int* __restrict__ score, long long n, int p, long long batch) {
+    nwk::nw_borders_body(score, n, p, batch);
+}

@@ -1,42 +1,13 @@
-// wavefront.cu -- Needleman-Wunsch score matrix as an anti-diagonal wavefront
-// (BASELINE.json config 4b).
-//
-//   S[0][j] = -j*p,  S[i][0] = -i*p,
-//   S[i][j] = max(S[i-1][j-1] + sim[i-1][j-1], S[i-1][j] - p, S[i][j-1] - p)
-//
-// Offset scores.  With S'[i][j] = S[i][j] + (i+j)*p the recurrence becomes
-//   S'[i][j] = max(S'[i-1][j-1] + sim[i-1][j-1] + 2p, S'[i-1][j], S'[i][j-1])
-// with all-zero borders: the left-to-right dependency chain is one integer
-// max per cell (no subtract), and the conversion back to S happens in the
-// store path, off the chain.  Exact whenever |p|*(2n+2) < 2^30 and the true
-// scores fit in +-2^30 (checked on p; sim is the caller's contract).
-//
-// Decomposition (no host loop over diagonals, no grid sync):
-//  * the n columns are cut into 128-wide strips, one CTA per strip, claimed in
-//    order from an atomic ticket (a strip's left neighbour is always already
-//    running); a persistent grid of at most one CTA per SM;
-//  * four warp roles per CTA, one per SM sub-partition:
-//      warp 0  compute:  sweeps the strip anti-diagonally over 4x4 cell blocks
-//              -- lane j owns columns 4j..4j+3 and at step s computes rows
-//              4(s-j) .. 4(s-j)+3, i.e. each step is one anti-diagonal of the
-//              (row quads x 32 lane-columns) grid, the LEGO antidiag order of
-//              the paper's NW kernel.  The four left
-//              values arrive by one warp shuffle each; everything else is in
-//              registers or 16-byte shared loads prefetched two steps ahead;
-//      warp 1  producer: cp.async-stages sim, 32 rows x 128 columns per
-//              block, into a 12-block ring (the compute warp overwrites each
-//              sim row with its S' row in place);
-//      warp 2  boundary: polls the left strip's published last column
-//              (32-bit words in global memory, preset to a sentinel no
-//              offset score can take) and hands it in row order, through a
-//              shared ring and a row counter, to compute lane 0;
-//      warp 3  flusher:  converts finished blocks S' -> S and writes them
-//              out as coalesced row segments;
-//  * roles synchronise through monotonic block counters in shared memory
-//    (loaded / computed / flushed); the compute warp checks them once per
-//    32 rows with a prefetched load, so its step body has no barrier.
+// wavefront.cu -- host side of the Needleman-Wunsch wavefront (BASELINE.json
+// config 4b) and the library's built-in instance of the kernel template
+// (nw_kernels.cuh) for the default layout: column strips of 128 columns
+// (tile order row-major over a 1 x ceil(n/128) tile grid, row-major ring).
+// Programs generated from other LEGO layouts (kernels.nw_program) are
+// compiled from the same template by NVRTC and launched through
+// lego_nw_run (lego_runtime.cu), sharing lego_nw_prepare below.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -46,493 +17,13 @@
 
 #include "lego_common.h"
 
-namespace {
-
-constexpr int CPL = 4;                               // columns per lane
-constexpr int STRIP = 32 * CPL;                      // columns per strip
-constexpr int BLK = 32;                              // rows per block
-#ifndef NW_RPS
-#define NW_RPS 4                                     // rows per lane per step
-#endif
-constexpr int RPS = NW_RPS;
-constexpr int STEPS = BLK / RPS;                     // compute steps per block
-constexpr int BLAG = (31 + STEPS - 1) / STEPS + 1;   // lane 31 completes block k before block k+BLAG starts
-constexpr int DRAIN = (31 + STEPS - 1) / STEPS;      // extra blocks cover lane 31's 31-step lag
-#ifndef NW_GRP
-#define NW_GRP (16 / NW_RPS)                         // measured: 4 steps 1068 us, 2 steps 1075, 1 step 1126 (n = 16384)
-#endif
-constexpr int GRP = NW_GRP;                          // boundary readiness checked every GRP steps
-constexpr int NSLOT = 12;                            // ring blocks
-constexpr int RING_ROWS = NSLOT * BLK;               // 384
-constexpr int BND_ROWS = 256;                        // boundary ring (rows)
-constexpr int BND_GROUPS = BND_ROWS / BLK;
-constexpr int ROW_BYTES = STRIP * 4;                 // 512
-constexpr int RING_BYTES = RING_ROWS * ROW_BYTES;    // 192 KiB
-constexpr int BND_BYTES = BND_ROWS * 4;
-constexpr int MBAR_BYTES = NSLOT * 8;
-constexpr int CTRL_BYTES = 64;
-constexpr int SMEM_BYTES = RING_BYTES + BND_BYTES + MBAR_BYTES + CTRL_BYTES;
-#ifndef NW_PRODUCER_NS
-#define NW_PRODUCER_NS 64                            // producer back-off when nothing landed or was issued
-#endif
-#ifndef NW_FLUSHER_NS
-#define NW_FLUSHER_NS 64                             // flusher back-off while waiting for a computed block
-#endif
-#ifndef NW_POLL_NS
-#define NW_POLL_NS 32                                // boundary poll back-off (measured: 32 ns 1068 us, 0 ns 1079 us)
-#endif
+#define NW_GLOBAL static __global__
+#include "nw_kernels.cuh"
 
 #ifdef LEGO_NW_DEBUG
-// progress probes written to mapped host memory (readable while the kernel runs):
-// dbg[(cta * 4 + warp) * 32 + lane] = last recorded position of that thread
-__device__ volatile int* g_nw_dbg;
-#define NW_PROBE(v) (g_nw_dbg[(blockIdx.x * 4 + (threadIdx.x >> 5)) * 32 + (threadIdx.x & 31)] = (v))
-// event times (globaltimer ns, low 32 bits): g_nw_trace[(cta * 4 + role) * 2048 + idx]
-__device__ unsigned g_nw_trace[148 * 4 * 2048];
-__device__ __forceinline__ unsigned nw_now() {
-    unsigned t;
-    asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(t));
-    return t;
-}
-__device__ __forceinline__ void g_nw_trace_strip(int strip) { g_nw_trace[(blockIdx.x * 4 + 3) * 2048 + 2047] = strip + 1; }
-#define NW_TRACE(role, idx) \
-    do { if ((idx) < 2048) g_nw_trace[(blockIdx.x * 4 + (role)) * 2048 + (idx)] = nw_now(); } while (0)
-#else
-#define NW_PROBE(v) ((void)0)
-#define NW_TRACE(role, idx) ((void)0)
-#define g_nw_trace_strip(s) ((void)0)
-#endif
-
-struct Ctrl {
-    int strip;
-    int loaded;      // sim blocks <= loaded have landed
-    int computed;    // S' blocks <= computed are final
-    int flushed;     // blocks <= flushed are written out (ring slot reusable)
-    int ready;       // boundary rows < ready are in the shared ring
-};
-
-// role counters in shared memory.  Publication is a release store at CTA
-// scope (the guarded data was written before it, after a __syncwarp); the
-// helper warps read counters with acquire loads.  The compute warp's hot
-// loop polls `ready` / `loaded` with plain volatile loads: an acquire there
-// costs 4 % of the kernel (1121 vs 1075 us at n = 16384), and the shared-
-// memory accesses of one SM's warps are performed in issue order by its one
-// shared-memory pipeline, which is what the pattern relies on.
-__device__ __forceinline__ int ldv(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
-__device__ __forceinline__ int ldv_acq(const int* p) {
-    int v;
-    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v)
-                 : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
-    return v;
-}
-__device__ __forceinline__ void stv(int* p, int v) {
-    asm volatile("st.release.cta.shared.b32 [%0], %1;" :: "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v)
-                 : "memory");
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
-
-// boundary words start as NW_EMPTY (|S'| < 2^30 never equals it)
-constexpr int NW_EMPTY = (int)0x80808080;
-__device__ __forceinline__ int ld_bnd(const int* p) {
-    int w;
-    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(w) : "l"(p) : "memory");
-    return w;
-}
-
-__global__ void nw_borders(int32_t* __restrict__ score, long long n, int p, long long batch) {
-    const long long w = n + 1;
-    const long long total = batch * w;
-    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
-         k += (long long)gridDim.x * blockDim.x) {
-        const long long b = k / w, x = k - b * w;
-        int32_t* s = score + b * w * w;
-        s[x] = (int32_t)(-x * p);          // row 0
-        s[x * w] = (int32_t)(-x * p);      // column 0
-    }
-}
-
-// compute-warp state: S' of the lane's 4 columns in its last finished row,
-// the diagonal predecessor of its first column, the last-column values it
-// sends right, and sim rows prefetched two steps ahead
-struct Lane {
-    int h[CPL];
-    int dprev;
-    int send[RPS];
-    int4 nx1[RPS], nx2[RPS];
-    int bv[RPS];
-};
-
-template <int N>
-__device__ __forceinline__ void ldsv(uint32_t a, int (&v)[N]);
-template <>
-__device__ __forceinline__ void ldsv<2>(uint32_t a, int (&v)[2]) {
-    asm volatile("ld.volatile.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(a));
-}
-template <>
-__device__ __forceinline__ void ldsv<4>(uint32_t a, int (&v)[4]) {
-    asm volatile("ld.volatile.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
-                 : "r"(a));
-}
-
-// predicated (branch-free) publication of RPS consecutive boundary words
-__device__ __forceinline__ void publish(int* p, int pred, const int (&v)[RPS]) {
-#if NW_RPS == 4
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\t"
-        "@q st.relaxed.gpu.global.v4.b32 [%0], {%2, %3, %4, %5};\n\t}"
-        :: "l"(p), "r"(pred), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]) : "memory");
-#else
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\t"
-        "@q st.relaxed.gpu.global.v2.b32 [%0], {%2, %3};\n\t}"
-        :: "l"(p), "r"(pred), "r"(v[0]), "r"(v[1]) : "memory");
-#endif
-}
-
-// one anti-diagonal step of the compute warp: lane j computes the RPS x 4
-// block rows r0 = RPS(s-j) .. r0+RPS-1, columns 4j..4j+3 of the strip
-__device__ __forceinline__ int ring_wrap(int r) { return r >= RING_ROWS ? r - RING_ROWS : r; }
-__device__ __forceinline__ int ring_mod(int r) {
-    int m = r % RING_ROWS;
-    return m < 0 ? m + RING_ROWS : m;
-}
-
-// rm = r0 mod RING_ROWS (RPS | RING_ROWS, so rows r0 .. r0+RPS-1 never straddle the wrap)
-template <bool GUARD>
-__device__ __forceinline__ void nw_step(Lane& c, int s, int lane, int4* ring_lane, uint32_t bnd, int p2, int n,
-                                        int* pub_row, int rm) {
-    const int r0 = RPS * (s - lane);
-    int4* cur_p = ring_lane + (rm << 5);
-    const int4* pf_p = ring_lane + (ring_wrap(rm + 2 * RPS) << 5);
-    int4 cur[RPS];
-    int lb[RPS];
-#pragma unroll
-    for (int q = 0; q < RPS; ++q) {
-        cur[q] = c.nx1[q];
-        c.nx1[q] = c.nx2[q];
-#ifndef NW_ABL_NOLDS
-        c.nx2[q] = pf_p[q * (STRIP / 4)];
-#else
-        c.nx2[q] = make_int4(q, lane, s, q ^ lane);
-#endif
-        lb[q] = c.bv[q];
-    }
-    ldsv<RPS>(bnd + (uint32_t)(((RPS * (s + 1)) & (BND_ROWS - 1)) * 4), c.bv);   // next step's boundary
-    int left[RPS];
-#pragma unroll
-    for (int q = 0; q < RPS; ++q) {
-#ifndef NW_ABL_NOSHFL
-        const int sl = __shfl_up_sync(0xffffffffu, c.send[q], 1);
-#else
-        const int sl = c.send[q] + q;                   // ablation: no lane exchange (wrong results)
-#endif
-        left[q] = lane == 0 ? lb[q] : sl;
-    }
-    const bool live = !GUARD || r0 >= 0;                // lanes start one step apart
-    int up0 = c.h[0], up1 = c.h[1], up2 = c.h[2], up3 = c.h[3];
-    int d = c.dprev;
-#pragma unroll
-    for (int q = 0; q < RPS; ++q) {
-        const int x0 = max(max(cur[q].x + d + p2, up0), left[q]);
-        const int x1 = max(max(cur[q].y + up0 + p2, up1), x0);
-        const int x2 = max(max(cur[q].z + up1 + p2, up2), x1);
-        const int x3 = max(max(cur[q].w + up2 + p2, up3), x2);
-#ifndef NW_ABL_NOSTS
-        if (live) cur_p[q * (STRIP / 4)] = make_int4(x0, x1, x2, x3);   // S' replaces sim in place
-#endif
-        up0 = x0; up1 = x1; up2 = x2; up3 = x3;
-        d = left[q];
-        c.send[q] = live ? x3 : c.send[q];
-    }
-    c.h[0] = live ? up0 : c.h[0];
-    c.h[1] = live ? up1 : c.h[1];
-    c.h[2] = live ? up2 : c.h[2];
-    c.h[3] = live ? up3 : c.h[3];
-    c.dprev = live ? d : c.dprev;
-    // the strip's last column goes to the right neighbour (lane 31, rows < n)
-    const int pub = (lane == 31) & (r0 < n) & live;
-#ifndef NW_ABL_NOPUB
-    publish(pub_row, pub, c.send);
-#endif
-}
-
-// one block of STEPS steps (32 rows of lane 0); boundary readiness is checked
-// every GRP steps against a counter value prefetched GRP steps earlier
-template <bool GUARD>
-__device__ __forceinline__ void nw_block(Lane& c, int k, int lane, int4* ring_lane, uint32_t bnd, int p2, int n,
-                                         int* my_bnd, int& rd, const int* ready, int rows_total) {
-    int* pub_blk = my_bnd + RPS * (k * STEPS - lane);  // lane 31's rows of step u: + RPS*u
-    int rm = ring_mod(k * BLK - RPS * lane);
-#pragma unroll
-    for (int u = 0; u < STEPS; ++u) {
-        const int s = k * STEPS + u;
-        if (u % GRP == 0) {                             // rows used (and prefetched) through step s + GRP
-            const int need = min(RPS * (s + GRP + 1), rows_total);   // the helper stops at rows_total
-            while (rd < need) rd = ldv(ready);
-            rd = ldv(ready);
-        }
-        nw_step<GUARD>(c, s, lane, ring_lane, bnd, p2, n, pub_blk + RPS * u, rm);
-        rm = ring_wrap(rm + RPS);
-    }
-}
-
-__global__ void __launch_bounds__(128, 1)
-nw_strips(const int32_t* __restrict__ sim, int32_t* __restrict__ score, int n, int p, int strips_per_matrix,
-          int total_strips, int* __restrict__ ticket, int* __restrict__ bnd_g) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    int32_t* ring_gen = reinterpret_cast<int32_t*>(smem);
-    Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem + RING_BYTES + BND_BYTES + MBAR_BYTES);
-    const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    const uint32_t bnd = ring + RING_BYTES;
-    const uint32_t mbar = bnd + BND_BYTES;
-    int gblk = 0;                                    // producer: blocks issued in earlier strips
-    if (threadIdx.x < NSLOT)
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" :: "r"(mbar + 8u * threadIdx.x) : "memory");
-    const int lane = threadIdx.x & 31;
-    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);   // warp-uniform role
-    const int n_pad = (n + BLK - 1) / BLK * BLK;
-    const int nblocks = n_pad / BLK;
-
-    for (;;) {
-        if (threadIdx.x == 0) {
-            ctrl->strip = atomicAdd(ticket, 1);
-            ctrl->loaded = ctrl->computed = ctrl->flushed = -1;
-            ctrl->ready = 0;
-        }
-        __syncthreads();
-        const int strip = ctrl->strip;
-        NW_PROBE(6000000 + strip);
-        if (threadIdx.x == 0) NW_TRACE(1, 2047 - 0 * strip);
-        if (threadIdx.x == 0 && strip < total_strips) g_nw_trace_strip(strip);
-        if (strip >= total_strips) return;
-        const int bm = strip / strips_per_matrix;
-        const int w = strip - bm * strips_per_matrix;
-        const int col0 = w * STRIP;
-        int* my_bnd = bnd_g + (long long)strip * n_pad;
-
-        if (warp == 0) {
-            // ---------------- compute ----------------
-            Lane c;
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) c.h[q] = 0;
-#pragma unroll
-            for (int q = 0; q < RPS; ++q) c.send[q] = 0;
-            c.dprev = 0;
-            const int p2 = 2 * p;
-            int4* ring4 = reinterpret_cast<int4*>(smem);
-            int pl = ldv(&ctrl->loaded);
-            int rd = ldv(&ctrl->ready);
-            for (int k = 0; k < nblocks + DRAIN; ++k) {
-                NW_PROBE(1000000 + k);
-                if (lane == 0) NW_TRACE(0, k);
-                if (k >= BLAG) {                        // lane 31 has finished block k - BLAG
-                    __syncwarp();
-                    if (lane == 0) stv(&ctrl->computed, k - BLAG);
-                }
-                // the last steps of block k prefetch block k+1's first rows: need both
-                const int need_blk = min(k + 1, nblocks + DRAIN - 1);
-                while (pl < need_blk) pl = ldv(&ctrl->loaded);
-                if (k == 0) {                           // operands of the first two steps
-                    while (rd < RPS) rd = ldv(&ctrl->ready);
-#pragma unroll
-                    for (int q = 0; q < RPS; ++q) {
-                        c.nx1[q] = ring4[ring_mod(-RPS * lane + q) * (STRIP / 4) + lane];
-                        c.nx2[q] = ring4[ring_mod(RPS - RPS * lane + q) * (STRIP / 4) + lane];
-                    }
-                    ldsv<RPS>(bnd, c.bv);
-                }
-                pl = ldv(&ctrl->loaded);                // prefetch for the next block
-                if (k < (31 + STEPS - 1) / STEPS)
-                    nw_block<true>(c, k, lane, ring4 + lane, bnd, p2, n, my_bnd, rd, &ctrl->ready, (nblocks + DRAIN) * BLK);
-                else
-                    nw_block<false>(c, k, lane, ring4 + lane, bnd, p2, n, my_bnd, rd, &ctrl->ready, (nblocks + DRAIN) * BLK);
-            }
-            __syncwarp();
-            if (lane == 0) stv(&ctrl->computed, nblocks + DRAIN - 1);
-        } else if (warp == 1) {
-            // ---------------- producer: sim blocks -> ring ----------------
-            // Issues block k once its ring slot is flushed; each block's
-            // copies arrive on a per-slot mbarrier, polled without blocking so
-            // `loaded` is published as soon as a block lands.
-            const int32_t* simb = sim + (long long)bm * n * n;
-            const bool vec = (n & 3) == 0;
-            const int total_blocks = nblocks + DRAIN;
-            int issued = 0, landed = 0;
-            while (landed < total_blocks) {
-                bool progress = false;
-                if (issued < total_blocks && (issued < NSLOT || ldv_acq(&ctrl->flushed) >= issued - NSLOT)) {
-                    const int k = issued;
-                    const uint32_t mb = mbar + 8u * (uint32_t)((gblk + k) % NSLOT);
-                    if (k < nblocks) {
-                        const int rows = min(BLK, n - k * BLK);
-                        uint32_t dst = ring + (uint32_t)((k % NSLOT) * BLK * ROW_BYTES);
-                        if (vec) {
-                            const bool ok = col0 + CPL * lane < n;
-                            const int32_t* src = simb + (long long)k * BLK * n + col0 + CPL * lane;
-                            dst += 16u * lane;
-#pragma unroll 8
-                            for (int r = 0; r < rows; ++r) {
-                                if (ok) cp_async16(dst, src);
-                                dst += ROW_BYTES;
-                                src += n;
-                            }
-                        } else {
-                            const int32_t* src = simb + (long long)k * BLK * n + col0 + lane;
-                            dst += 4u * lane;
-                            for (int r = 0; r < rows; ++r) {
-#pragma unroll
-                                for (int q = 0; q < CPL; ++q)
-                                    if (col0 + 32 * q + lane < n) cp_async4(dst + 128u * q, src + 32 * q);
-                                dst += ROW_BYTES;
-                                src += n;
-                            }
-                        }
-                        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(mb) : "memory");
-                    } else {
-                        asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}"
-                                     :: "r"(mb) : "memory");
-                    }
-                    ++issued;
-                    progress = true;
-                }
-                if (landed < issued) {
-                    const int g = gblk + landed;
-                    uint32_t ok;
-                    asm volatile("{\n\t.reg .pred p;\n\t"
-                                 "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                                 "selp.u32 %0, 1, 0, p;\n\t}"
-                                 : "=r"(ok) : "r"(mbar + 8u * (uint32_t)(g % NSLOT)), "r"((g / NSLOT) & 1)
-                                 : "memory");
-                    if (__all_sync(0xffffffffu, ok)) {
-                        if (lane == 0) {
-                            stv(&ctrl->loaded, landed);
-                            NW_TRACE(1, landed);
-                        }
-                        ++landed;
-                        progress = true;
-                    }
-                }
-                if (!progress) __nanosleep(NW_PRODUCER_NS);
-            }
-            gblk += total_blocks;
-        } else if (warp == 2) {
-            // ---------------- boundary: left strip's last column -> shared ring ----------------
-            // Lane l polls row 32m + l; rows are handed to the compute warp in
-            // order through ctrl->ready as soon as a prefix of the group is in.
-            const int* left = my_bnd - n_pad;
-            const int groups = nblocks + DRAIN;
-            for (int m = 0; m < groups; ++m) {
-                const int r = m * BLK + lane;
-                NW_PROBE(3000000 + r);
-                if (m >= BND_GROUPS) {
-                    while (ldv_acq(&ctrl->computed) < m - BND_GROUPS) __nanosleep(128);
-                }
-                int v = 0;                              // S'[r+1][0] = 0 on the matrix edge
-                bool ok = true;
-                if (w > 0 && r < n) {
-                    v = ld_bnd(left + r);
-                    ok = v != NW_EMPTY;
-                }
-                bool written = false;
-                int told = 0;
-                for (;;) {
-                    const unsigned ball = __ballot_sync(0xffffffffu, ok);
-                    const int t = ball == 0xffffffffu ? 32 : __ffs(~ball) - 1;   // ready prefix
-                    if (ok && !written && lane < t) {
-                        asm volatile("st.shared.b32 [%0], %1;" :: "r"(bnd + (uint32_t)((r & (BND_ROWS - 1)) * 4)),
-                                     "r"(v) : "memory");
-                        written = true;
-                    }
-                    if (t > told) {
-                        __syncwarp();
-                        if (lane == 0) stv(&ctrl->ready, m * BLK + t);
-                        told = t;
-                    }
-                    if (t == 32) break;
-                    if (NW_POLL_NS) __nanosleep(NW_POLL_NS);
-                    if (!ok) {
-                        v = ld_bnd(left + r);
-                        ok = v != NW_EMPTY;
-                    }
-                }
-                if (lane == 31) NW_TRACE(2, m);
-            }
-        } else {
-            // ---------------- flusher: S' -> S, coalesced row segments ----------------
-            int32_t* sc = score + (long long)bm * ((long long)n + 1) * ((long long)n + 1);
-            const long long ld = (long long)n + 1;
-            bool ok[CPL];
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) ok[q] = col0 + 32 * q + lane < n;
-            for (int k = 0; k < nblocks; ++k) {
-                NW_PROBE(5000000 + k);
-                while (ldv_acq(&ctrl->computed) < k) __nanosleep(NW_FLUSHER_NS);
-                const int rows = min(BLK, n - k * BLK);
-                const int32_t* src = ring_gen + (k % NSLOT) * BLK * STRIP + lane;
-                int32_t* dst = sc + (long long)(k * BLK + 1) * ld + col0 + 1 + lane;
-                int off = (k * BLK + col0 + lane + 2) * p;     // (i + j) * p of column lane, row k*BLK
-                if (rows == BLK && col0 + STRIP <= n) {
-                    // full block: 16 rows of loads in flight before their stores
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        int v[16][CPL];
-#pragma unroll
-                        for (int r = 0; r < 16; ++r)
-#pragma unroll
-                            for (int q = 0; q < CPL; ++q) v[r][q] = src[(16 * h + r) * STRIP + 32 * q];
-#pragma unroll
-                        for (int r = 0; r < 16; ++r) {
-                            int32_t* d = dst + (16 * h + r) * ld;
-                            const int o = off + (16 * h + r) * p;
-#pragma unroll
-                            for (int q = 0; q < CPL; ++q) d[32 * q] = v[r][q] - (o + 32 * q * p);
-                        }
-                    }
-                } else {
-#pragma unroll 4
-                for (int r = 0; r < rows; ++r) {
-#pragma unroll
-                    for (int q = 0; q < CPL; ++q)
-                        if (ok[q]) dst[32 * q] = src[32 * q] - (off + 32 * q * p);
-                    dst += ld;
-                    src += STRIP;
-                    off += p;
-                }
-                }
-                __syncwarp();
-                if (lane == 0) { stv(&ctrl->flushed, k); NW_TRACE(3, k); }
-            }
-        }
-        __syncthreads();
-    }
-}
-
-}  // namespace
-
-#ifdef LEGO_NW_DEBUG
-static int* lego_nw_dbg_host = nullptr;
-static void* g_nw_trace_ptr() {
-    void* p = nullptr;
-    cudaGetSymbolAddress(&p, g_nw_trace);
-    return p;
-}
-// snapshot of the progress probes (debug builds only)
+// snapshot of the per-role event times (debug builds only)
 extern "C" int lego_nw_debug_trace(unsigned* out) {
-    return cudaMemcpyFromSymbol(out, g_nw_trace, sizeof(g_nw_trace)) == cudaSuccess ? 148 * 4 * 2048 : 0;
-}
-extern "C" int lego_nw_debug_snapshot(int* out, int count) {
-    if (!lego_nw_dbg_host) return 0;
-    const int m = count < 148 * 4 * 32 ? count : 148 * 4 * 32;
-    for (int i = 0; i < m; ++i) out[i] = ((volatile int*)lego_nw_dbg_host)[i];
-    return m;
+    return cudaMemcpyFromSymbol(out, nwk::g_nw_trace, sizeof(nwk::g_nw_trace)) == cudaSuccess ? 148 * 4 * 2048 : 0;
 }
 #endif
 
@@ -545,14 +36,14 @@ struct NwScratch {
 };
 constexpr size_t NW_TICKET_BYTES = 256;
 
-static lego_status nw_scratch(cudaStream_t st, size_t bnd_bytes, int** ticket, int** bnd) {
+static lego_status nw_scratch(cudaStream_t st, size_t words_bytes, int** ticket, int** words) {
     static std::mutex mu;
     static std::map<std::pair<int, cudaStream_t>, NwScratch> cache;
     int dev = 0;
     LEGO_TRY(lego_cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
     std::lock_guard<std::mutex> lk(mu);
     NwScratch& e = cache[std::make_pair(dev, st)];
-    const size_t need = NW_TICKET_BYTES + bnd_bytes;
+    const size_t need = NW_TICKET_BYTES + words_bytes;
     if (e.bytes < need) {
         if (e.buf) LEGO_TRY(lego_cuda_check(cudaFreeAsync(e.buf, st), "cudaFreeAsync"));
         e.buf = nullptr;
@@ -562,54 +53,86 @@ static lego_status nw_scratch(cudaStream_t st, size_t bnd_bytes, int** ticket, i
         e.bytes = grow;
     }
     LEGO_TRY(lego_cuda_check(cudaMemsetAsync(e.buf, 0, NW_TICKET_BYTES, st), "cudaMemsetAsync"));
-    LEGO_TRY(lego_cuda_check(cudaMemsetAsync(e.buf + NW_TICKET_BYTES, 0x80, bnd_bytes, st), "cudaMemsetAsync"));
+    if (words_bytes)
+        LEGO_TRY(lego_cuda_check(cudaMemsetAsync(e.buf + NW_TICKET_BYTES, 0x80, words_bytes, st),
+                                 "cudaMemsetAsync"));
     *ticket = reinterpret_cast<int*>(e.buf);
-    *bnd = reinterpret_cast<int*>(e.buf + NW_TICKET_BYTES);
+    *words = reinterpret_cast<int*>(e.buf + NW_TICKET_BYTES);
+    return LEGO_OK;
+}
+
+int lego_nw_smem_bytes() { return nwk::SMEM_BYTES; }
+
+lego_status lego_nw_prepare(const int32_t* sim, int32_t* score, int64_t n, int32_t penalty, int64_t batch,
+                            int64_t tile_rows, int tiled, cudaStream_t st, NwPlan* plan) {
+    memset(plan, 0, sizeof *plan);
+    if (n < 0 || batch < 0) return lego_fail(LEGO_E_SHAPE, "negative NW size");
+    if (n > (1 << 20)) return lego_fail(LEGO_E_SHAPE, "NW n above 2^20");
+    if (batch == 0) return LEGO_OK;
+    if (!score || (n > 0 && !sim)) return lego_fail(LEGO_E_ARG, "null buffer");
+    if ((uintptr_t)sim & 15) return lego_fail(LEGO_E_ARG, "sim must be 16-byte aligned");
+    if ((uintptr_t)score & 3) return lego_fail(LEGO_E_ARG, "score must be 4-byte aligned");
+    if ((long long)std::llabs((long long)penalty) * (2 * n + 2) >= (1LL << 30))
+        return lego_fail(LEGO_E_ARG, "|penalty| * (2n + 2) must stay below 2^30 (offset scores are int32)");
+    plan->n = n;
+    plan->batch = batch;
+    const long long bgrid = (batch * (n + 1) + 255) / 256;
+    plan->border_ctas = (unsigned)(bgrid < 4096 ? bgrid : 4096);
+    if (n == 0) return LEGO_OK;
+    const long long H = tile_rows > 0 ? tile_rows : n;
+    const long long nr = (n + H - 1) / H;
+    const long long nc = (n + nwk::STRIP - 1) / nwk::STRIP;
+    if (nr > 1 && (H % nwk::BLK)) return lego_fail(LEGO_E_SHAPE, "tile rows must be a multiple of 32");
+    if (nr > 1 && !tiled) return lego_fail(LEGO_E_ARG, "a strip program cannot run tiles of %lld rows", H);
+    const long long total = nr * nc * batch;
+    if (total > INT32_MAX / 2) return lego_fail(LEGO_E_SHAPE, "NW batch too large");
+    const long long n_pad = (n + nwk::BLK - 1) / nwk::BLK * nwk::BLK;
+    const size_t bnd_words = (size_t)(nc * batch) * (size_t)n_pad;
+    const size_t top_words = tiled ? (size_t)total * nwk::STRIP : 0;
+    int* ticket = nullptr;
+    int* words = nullptr;
+    LEGO_TRY(nw_scratch(st, sizeof(int) * (bnd_words + top_words), &ticket, &words));
+    int dev = 0, sms = 148;
+    LEGO_TRY(lego_cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    plan->H = (int)H;
+    plan->nr = (int)nr;
+    plan->nc = (int)nc;
+    plan->total = (int)total;
+    plan->ticket = ticket;
+    plan->bnd = words;
+    plan->top = tiled ? words + bnd_words : nullptr;
+    plan->ctas = (unsigned)(total < sms ? total : sms);     // one CTA per SM, persistent
+    plan->smem = nwk::SMEM_BYTES;
     return LEGO_OK;
 }
 
 extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n, int32_t penalty, int64_t batch,
                                    void* stream) {
-    if (n < 0 || batch < 0) return lego_fail(LEGO_E_SHAPE, "negative NW size");
-    if (batch == 0) return LEGO_OK;
-    if (n > (1 << 20)) return lego_fail(LEGO_E_SHAPE, "NW n above 2^20");
-    if (!score || (n > 0 && !sim)) return lego_fail(LEGO_E_ARG, "null buffer");
-    if ((uintptr_t)sim & 15) return lego_fail(LEGO_E_ARG, "sim must be 16-byte aligned");
-    if ((long long)std::llabs((long long)penalty) * (2 * n + 2) >= (1LL << 30))
-        return lego_fail(LEGO_E_ARG, "|penalty| * (2n + 2) must stay below 2^30 (offset scores are int32)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const long long w = n + 1;
-    const long long bgrid = (batch * w + 255) / 256;
-    nw_borders<<<(unsigned)(bgrid < 4096 ? bgrid : 4096), 256, 0, st>>>(score, n, penalty, batch);
+    NwPlan pl;
+    LEGO_TRY(lego_nw_prepare(sim, score, n, penalty, batch, n, 0, st, &pl));
+    if (batch == 0) return LEGO_OK;
+    lego_nw_borders<<<pl.border_ctas, 256, 0, st>>>(score, n, penalty, batch);
     if (n == 0) return lego_cuda_check(cudaGetLastError(), "nw borders");
-    const int strips = (int)((n + STRIP - 1) / STRIP);
-    const long long total = (long long)strips * batch;
-    if (total > INT32_MAX) return lego_fail(LEGO_E_SHAPE, "NW batch too large");
-    const long long n_pad = (n + BLK - 1) / BLK * BLK;
-    const size_t bnd_bytes = sizeof(int) * (size_t)total * (size_t)n_pad;
-    int* ticket = nullptr;
-    int* bnd_g = nullptr;
-    LEGO_TRY(nw_scratch(st, bnd_bytes, &ticket, &bnd_g));
-    static cudaError_t attr = cudaFuncSetAttribute(nw_strips, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   SMEM_BYTES);
-    LEGO_TRY(lego_cuda_check(attr, "cudaFuncSetAttribute(nw)"));
-#ifdef LEGO_NW_DEBUG
-    static int* host_dbg = nullptr;
-    if (!host_dbg) {
-        cudaHostAlloc((void**)&host_dbg, 148 * 4 * 32 * sizeof(int), cudaHostAllocMapped);
-        int* dptr = nullptr;
-        cudaHostGetDevicePointer((void**)&dptr, host_dbg, 0);
-        cudaMemcpyToSymbol(g_nw_dbg, &dptr, sizeof(dptr));
-        lego_nw_dbg_host = host_dbg;
+    // the >48 KiB dynamic shared memory opt-in is a per-device function attribute
+    static std::atomic<unsigned long long> attr_set{0};
+    int dev = 0;
+    LEGO_TRY(lego_cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_set.load() & bit)) {
+        LEGO_TRY(lego_cuda_check(cudaFuncSetAttribute(lego_nw_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      nwk::SMEM_BYTES), "cudaFuncSetAttribute(nw)"));
+        attr_set.fetch_or(bit);
     }
-    memset(host_dbg, 0xff, 148 * 4 * 32 * sizeof(int));
-    cudaMemsetAsync(g_nw_trace_ptr(), 0, 148 * 4 * 2048 * sizeof(unsigned), st);
+#ifdef LEGO_NW_DEBUG
+    {
+        void* trace = nullptr;
+        cudaGetSymbolAddress(&trace, nwk::g_nw_trace);
+        cudaMemsetAsync(trace, 0, sizeof(nwk::g_nw_trace), st);
+    }
 #endif
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long ctas = total < sms ? total : sms;      // one strip CTA per SM, persistent
-    nw_strips<<<(unsigned)ctas, 128, SMEM_BYTES, st>>>(sim, score, (int)n, penalty, strips, (int)total, ticket,
-                                                       bnd_g);
+    lego_nw_tiles<<<pl.ctas, 128, pl.smem, st>>>(sim, score, (int)n, penalty, pl.H, pl.nr, pl.nc, pl.total,
+                                                  pl.ticket, pl.bnd, pl.top);
     return lego_cuda_check(cudaGetLastError(), "nw launch");
 }

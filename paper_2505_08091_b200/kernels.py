@@ -608,22 +608,50 @@ def softmax(x, *, out=None, stream=None):
     return out
 
 
-def nw_score(sim, penalty: int, *, out=None, stream=None):
-    """Needleman-Wunsch score matrices for int32 similarity ``(..., n, n)``."""
+def nw_score(sim, penalty: int, *, layout=None, out=None, stream=None):
+    """Needleman-Wunsch score matrices for int32 similarity ``(..., n, n)``.
+
+    ``layout`` is a LEGO layout of the n x n cell grid (:func:`.nw.nw_layout`)
+    whose tile order and shared-memory cell order drive the wavefront kernel
+    (:mod:`.nw`); ``None`` runs the library's built-in instance of the default
+    layout (128-column strips)."""
     torch = _torch()
-    if sim.dtype != torch.int32 or not sim.is_cuda or sim.shape[-1] != sim.shape[-2]:
+    if sim.dtype != torch.int32 or not sim.is_cuda or sim.dim() < 2 or sim.shape[-1] != sim.shape[-2]:
         raise ShapeMismatch("nw_score takes a CUDA int32 tensor of shape (..., n, n)")
     sim = sim.contiguous()
     n = sim.shape[-1]
     batch = 1
     for d in sim.shape[:-2]:
         batch *= d
+    shape = (*sim.shape[:-2], n + 1, n + 1)
     if out is None:
-        out = torch.empty(*sim.shape[:-2], n + 1, n + 1, dtype=torch.int32, device=sim.device)
-    runtime.check(runtime.lib().lego_nw_i32(sim.data_ptr(), out.data_ptr(), n, int(penalty), batch,
-                                            runtime.stream_handle(stream)), "lego_nw_i32")
-    LAUNCHES[0] += 1
+        out = torch.empty(*shape, dtype=torch.int32, device=sim.device)
+    else:
+        _check_out(out, shape, torch.int32, sim.device, "nw_score")
+    with torch.cuda.device(sim.device):
+        st = runtime.stream_handle(stream)
+        if layout is None or n == 0 or batch == 0:
+            runtime.check(runtime.lib().lego_nw_i32(sim.data_ptr(), out.data_ptr(), n, int(penalty), batch, st),
+                          "lego_nw_i32")
+        else:
+            from . import nw
+            prog = nw.nw_program(layout, n, device=sim.device)
+            runtime.check(runtime.lib().lego_nw_run(prog.prog.handle, sim.data_ptr(), out.data_ptr(), n,
+                                                    int(penalty), batch, st), "lego_nw_run")
+    LAUNCHES[0] += 2
     return out
+
+
+def _check_out(out, shape, dtype, device, what):
+    """Caller-provided outputs go to the C ABI as bare pointers: check them."""
+    if out.dtype != dtype:
+        raise ShapeMismatch(f"{what}: out has dtype {out.dtype}, expected {dtype}")
+    if out.device != device:
+        raise ShapeMismatch(f"{what}: out is on {out.device}, expected {device}")
+    if not out.is_contiguous():
+        raise ShapeMismatch(f"{what}: out must be contiguous")
+    if tuple(out.shape) != tuple(shape):
+        raise ShapeMismatch(f"{what}: out has shape {tuple(out.shape)}, expected {tuple(shape)}")
 
 
 # measured (scripts/ab_gemm_group.py, 8192^3, 4 alternating runs each): G = 32 685 us,

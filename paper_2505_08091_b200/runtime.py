@@ -49,7 +49,7 @@ class ProgramInfo(ctypes.Structure):
                 ("reserved", ctypes.c_int32)]
 
 
-KIND_INDEX_MAP, KIND_GATHER, KIND_TRANSPOSE, KIND_BAND, KIND_SCATTER, KIND_STAGED = 0, 1, 2, 3, 4, 5
+KIND_INDEX_MAP, KIND_GATHER, KIND_TRANSPOSE, KIND_BAND, KIND_SCATTER, KIND_STAGED, KIND_NW = 0, 1, 2, 3, 4, 5, 6
 # lego_program_info.reserved flags (include/lego_b200.h): element-aligned buffers suffice
 ALIGN_SRC_FREE, ALIGN_DST_FREE = 1, 2
 
@@ -76,6 +76,7 @@ SIGS = {
     "lego_remap": ([VP, VP, VP, I64, I64, I64, VP], I32),
     "lego_softmax_f32": ([VP, VP, I64, I64, VP], I32),
     "lego_nw_i32": ([VP, VP, I64, I32, I64, VP], I32),
+    "lego_nw_run": ([VP, VP, VP, I64, I32, I64, VP], I32),
     "lego_gemm_bf16": ([VP, VP, VP, I64, I64, I64, I64, I32, VP], I32),
     "lego_gemm_bf16_ex": ([VP, VP, VP, I64, I64, I64, I64, I32, I32, I32, VP], I32),
 }
