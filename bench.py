@@ -118,6 +118,8 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -125,6 +127,49 @@ def dist_setup(args):
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
+
+
+def self_launch(args) -> int:
+    """``--gpus N`` without a torchrun environment: start N ranks of this
+    script through torch.distributed.run on 127.0.0.1 (NCCL_DEBUG=INFO so
+    the communicator lines show N ranks) and return their exit code.  Rank
+    0's JSON line reaches stdout unchanged."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args):
+    """Rendezvous only (gloo, CPU): each rank reports the world it joined.
+    Lets CPU tests check the multi-rank launch without a GPU."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        dist.init_process_group("gloo")
+        got = dist.get_world_size()
+        import torch
+        t = torch.tensor([1])
+        dist.all_reduce(t)
+        ranks = int(t.item())
+        dist.destroy_process_group()
+    else:
+        got, ranks = 1, 1
+    sys.stderr.write(f"rank {rank} world={got}\n")
+    sys.stderr.flush()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": got, "ranks_joined": ranks,
+                          "workload": args.workload}), flush=True)
 
 
 def barrier(world):
@@ -391,6 +436,157 @@ def run(args):
         dist.destroy_process_group()
 
 
+def _pinned_e2e(world, h2d_pairs, d2h_pairs, compute, steps):
+    """End-to-end device time per step of: H2D of the inputs from pinned host
+    memory, the compute, D2H of the outputs, on the current stream."""
+    import torch
+    def one():
+        for dev, host in h2d_pairs:
+            dev.copy_(host, non_blocking=True)
+        compute()
+        for host, dev in d2h_pairs:
+            host.copy_(dev, non_blocking=True)
+    for _ in range(3):
+        one()
+    torch.cuda.synchronize()
+    barrier(world)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        one()
+    t1.record()
+    t1.synchronize()
+    return max_over_ranks(t0.elapsed_time(t1), world) / steps
+
+
+def run_gemm_b8(args):
+    """cfg5 as BASELINE.json states it: a batch of 8 bf16 8192^3 GEMMs
+    (C = A B^T, tcgen05), batch-sharded 8/N per GPU -- strong scaling, no
+    data-path collective."""
+    import torch
+
+    from paper_2505_08091_b200 import kernels as K, shard
+    world, rank, _local = dist_setup(args)
+    pk = peaks()
+    B, n = 8, 8192
+    p = shard.ShardPlan(B, world, rank)
+    a = torch.empty(p.count, n, n, dtype=torch.bfloat16, device="cuda")
+    b = torch.empty_like(a)
+    for i in range(p.count):
+        g = torch.Generator(device="cuda").manual_seed(5 + 2 * (p.start + i))
+        a[i] = torch.randn(n, n, generator=g, device="cuda").to(torch.bfloat16)
+        b[i] = torch.randn(n, n, generator=g, device="cuda").to(torch.bfloat16)
+    c = torch.empty_like(a)
+    step = lambda: K.gemm(a, b, out=c)  # noqa: E731
+    step()
+    ref = torch.matmul(a[0, :64].double(), b[0].double().T) if p.count else None
+    rel = 0.0
+    if ref is not None:
+        rel = ((c[0, :64].double() - ref).abs() / ref.abs().clamp_min(1e-2 * ref.abs().max().item())).max().item()
+    launches0 = K.LAUNCHES[0]
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        ms = time_steps(step, args.steps, args.warmup, world)
+    launches = K.LAUNCHES[0] - launches0 - args.warmup
+    ms_step = ms / args.steps
+    flops = 2 * n ** 3 * B
+    value = flops / (ms_step * 1e-3) / 1e12
+    per_gpu = 2 * n ** 3 * max(p.count, 1) / (ms_step * 1e-3) / 1e12
+    ha = torch.empty(a.shape, dtype=a.dtype, pin_memory=True)
+    hb = torch.empty(b.shape, dtype=b.dtype, pin_memory=True)
+    hc = torch.empty(c.shape, dtype=c.dtype, pin_memory=True)
+    ha.copy_(a)
+    hb.copy_(b)
+    e2e_ms = _pinned_e2e(world, [(a, ha), (b, hb)], [(hc, c)], step, max(3, args.steps // 4))
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        xa = a[0, :256].float().cpu()
+        xb = b[0].float().cpu()
+        torch.set_num_threads(len(os.sched_getaffinity(0)))
+        torch.matmul(xa[:16], xb.T)
+        t0 = time.perf_counter()
+        torch.matmul(xa, xb.T)
+        dt = time.perf_counter() - t0
+        cpu = {"value": round(2 * 256 * n * n / dt / 1e12, 4), "unit": "TFLOP/s", "cores": torch.get_num_threads(),
+               "kind": "port", "sample": f"256 rows of one 8192^3 GEMM, torch CPU fp32 matmul (restatement; the "
+                                         f"reference has no GEMM), {dt:.2f} s"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 1), "unit": "TFLOP/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (randn bf16, seeds 5+2k)",
+                "config": {"workload": "cfg5: batch of 8 bf16 8192x8192x8192 GEMMs (C = A B^T) on tcgen05, "
+                                       "batch-sharded 8/N per GPU", "per_gpu_matrices": p.count,
+                           "parallelism": f"strong: batch 8 split over {world} GPUs, no data-path collective",
+                           "l2": "no flush: 384 MiB of operands per GEMM >> 126 MB L2",
+                           "check_max_rel_64_rows": rel},
+                "roofline": {"bound": "tensor", "achieved": round(per_gpu, 1), "peak": pk["bf16"],
+                             "unit": "TFLOP/s", "frac": round(per_gpu / pk["bf16"], 4),
+                             "frac_sustained": round(per_gpu / pk["bf16_sustained"], 4), "traffic": None,
+                             "peak_source": pk["source"]},
+                "cpu_baseline": cpu,
+                "e2e": {"value": round(flops / (e2e_ms * 1e-3) / 1e12, 1), "unit": "TFLOP/s",
+                        "h2d_bytes_per_step": 2 * a.numel() * 2, "d2h_bytes_per_step": c.numel() * 2},
+                "gpu_launches": launches, "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_transpose_shard(args):
+    """cfg2 on ONE matrix split over N GPUs: rank r holds rows
+    [r*n/N, (r+1)*n/N) of the 16384^2 bf16 matrix and ends with its share of
+    the Col layout, through shard.FusedTranspose (one routed register
+    transpose per rank storing into the peers' symmetric-memory shards over
+    NVLink) -- strong scaling, the exchange fused into the remap kernel."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_08091_b200 import kernels as K, shard
+    world, rank, _local = dist_setup(args)
+    if world == 1:                      # symmetric memory needs a process group, even of one rank
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0,
+                                device_id=torch.device("cuda", 0))
+    n = N
+    R = n // world
+    g = torch.Generator(device="cuda").manual_seed(1 + rank)
+    rows = torch.randn(R, n, generator=g, device="cuda").to(torch.bfloat16)
+    ft = shard.FusedTranspose(n, n, rows.dtype, rows.device)
+    step = lambda: ft(rows)  # noqa: E731
+    out = step()
+    torch.cuda.synchronize()
+    C = n // world
+    ok = torch.equal(out[:, rank * R:(rank + 1) * R], rows[:, rank * C:(rank + 1) * C].T)
+    launches0 = K.LAUNCHES[0]
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        ms = time_steps(step, args.steps, args.warmup, world)
+    launches = K.LAUNCHES[0] - launches0 - args.warmup
+    ms_step = ms / args.steps
+    nbytes = 2 * n * n * 2
+    value = nbytes / (ms_step * 1e-3) / 1e9
+    pk = peaks()
+    per_gpu = nbytes / world / (ms_step * 1e-3) / 1e9
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (randn bf16)",
+                "config": {"workload": "cfg2 on one 16384x16384 bf16 matrix row-sharded over N GPUs -> Col layout "
+                                       "(shard.FusedTranspose: routed register transpose into NVLink peer shards)",
+                           "layout": HEADLINE_DSL, "check_own_block": "ok" if ok else "MISMATCH",
+                           "parallelism": f"strong: {world} row shards, exchange fused into the remap kernel"},
+                "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1), "peak": pk["hbm"], "unit": "GB/s",
+                             "frac": round(per_gpu / pk["hbm"], 4), "traffic": None,
+                             "note": "per-GPU bytes read + written; with N > 1, (N-1)/N of the writes cross NVLink"},
+                "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def lower_size(layout):
     from paper_2505_08091_b200 import lower
     return lower.physical_size(layout)
@@ -463,16 +659,20 @@ def other_kernels(args, pk, world):
     f4 = L.GroupBy([1 << 26], orders=(L.OrderBy(even),), injective=True)
     frow("f4_injective_even_scatter_i32", f4, 1 << 26, "to", scatter=True,
          traffic_key="remap_scatter_f4_i32")
-    # cfg4b: NW wavefront 16384^2 int32
+    # cfg4b: NW wavefront 16384^2 int32, driven by a LEGO layout of the cell grid
     try:
+        from paper_2505_08091_b200 import nw as NW
         sim = torch.randint(-10, 11, (16384, 16384), device="cuda", dtype=torch.int32)
         score = torch.empty(16385, 16385, device="cuda", dtype=torch.int32)
-        ms = time_steps(lambda: K.nw_score(sim, 10, out=score), 5, 3, world)
-        ms /= 5
         cells = 16384 * 16384
-        res["cfg4b_nw_wavefront_i32"] = {"GCUPS": round(cells / (ms * 1e-3) / 1e9, 1),
-                                         "us": round(ms * 1e3, 1),
-                                         "GB/s": round((cells * 4 + 16385 ** 2 * 4) / (ms * 1e-3) / 1e9, 1)}
+        nw_layouts = [("cfg4b_nw_wavefront_i32", NW.nw_layout(16384)),
+                      ("cfg4b_nw_tiles128_antidiag_i32", NW.nw_layout(16384, tile_rows=128, tile_order="antidiag"))]
+        for name, lay in nw_layouts:
+            K.nw_score(sim, 10, layout=lay, out=score)
+            ms = time_steps(lambda: K.nw_score(sim, 10, layout=lay, out=score), 5, 3, world) / 5
+            res[name] = {"GCUPS": round(cells / (ms * 1e-3) / 1e9, 1), "us": round(ms * 1e3, 1),
+                         "GB/s": round((cells * 4 + 16385 ** 2 * 4) / (ms * 1e-3) / 1e9, 1),
+                         "layout": NW.describe(lay), "path": "lego_nw_run (NVRTC program of the layout)"}
         del sim, score
     except Exception as exc:  # noqa: BLE001
         res["cfg4b_nw_wavefront_i32"] = {"unavailable": str(exc)[:200]}
@@ -499,11 +699,24 @@ def main():
     ap.add_argument("--impl", default="lego", choices=["lego", "reference"])
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="remap", choices=["remap", "gemm_b8", "transpose_shard"],
+                    help="remap: headline cfg2 (weak scaling, one matrix per GPU); gemm_b8: cfg5 batch of 8 "
+                         "8192^3 GEMMs split 8/N per GPU (strong); transpose_shard: one 16384^2 bf16 matrix "
+                         "row-sharded over N GPUs into the Col layout by the fused routed transpose (strong)")
+    ap.add_argument("--dry-run", action="store_true", help="launch and rendezvous only (CPU, gloo)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
+    elif args.workload == "gemm_b8":
+        run_gemm_b8(args)
+    elif args.workload == "transpose_shard":
+        run_transpose_shard(args)
     else:
         run(args)
 

@@ -159,26 +159,41 @@ def transpose_rows_fused(local_rows, n_rows: int, n_cols: int, *, group=None):
     writes, and every store has landed before anyone reads.  Same result as
     :func:`transpose_rows` (tests/test_shard.py checks the routing for every
     rank on CPU; tests/test_gpu_kernels.py runs the routed kernel on a GPU
-    against per-rank buffers)."""
-    import torch
-    from torch.distributed import _symmetric_memory as symm
-    from . import kernels
-    dist = _dist()
-    world, rank = world_and_rank(group)
+    against per-rank buffers).  Repeated calls should hold one
+    :class:`FusedTranspose` (the symmetric buffer is set up once)."""
+    world, _rank = world_and_rank(group)
     if n_rows % world or n_cols % world:
         raise ShapeMismatch(f"{n_rows}x{n_cols} does not split over {world} ranks")
-    R, C = n_rows // world, n_cols // world
-    if local_rows.shape != (R, n_cols):
-        raise ShapeMismatch(f"local rows {tuple(local_rows.shape)} != {(R, n_cols)}")
-    out = symm.empty((C, n_rows), dtype=local_rows.dtype, device=local_rows.device)
-    handle = symm.rendezvous(out, group if group is not None else dist.group.WORLD)
-    peers = torch.tensor([int(p) for p in handle.buffer_ptrs], dtype=torch.int64,
-                         device=local_rows.device)
-    layout, route = fused_transpose_route(R, C, world, rank)
-    handle.barrier(channel=0)
-    kernels.remap_routed(local_rows.reshape(-1), None, layout, peers, route)
-    handle.barrier(channel=0)
-    return out
+    ft = FusedTranspose(n_rows, n_cols, local_rows.dtype, local_rows.device, group=group)
+    return ft(local_rows)
+
+
+class FusedTranspose:
+    """Set-up of :func:`transpose_rows_fused` kept across calls: the
+    symmetric output shard, its peer address table and the routed program."""
+
+    def __init__(self, n_rows: int, n_cols: int, dtype, device, *, group=None):
+        import torch
+        from torch.distributed import _symmetric_memory as symm
+        dist = _dist()
+        world, rank = world_and_rank(group)
+        if n_rows % world or n_cols % world:
+            raise ShapeMismatch(f"{n_rows}x{n_cols} does not split over {world} ranks")
+        self.R, self.C, self.world, self.rank = n_rows // world, n_cols // world, world, rank
+        self.n_rows, self.n_cols = n_rows, n_cols
+        self.out = symm.empty((self.C, n_rows), dtype=dtype, device=device)
+        self.handle = symm.rendezvous(self.out, group if group is not None else dist.group.WORLD)
+        self.peers = torch.tensor([int(p) for p in self.handle.buffer_ptrs], dtype=torch.int64, device=device)
+        self.layout, self.route = fused_transpose_route(self.R, self.C, world, rank)
+
+    def __call__(self, local_rows):
+        from . import kernels
+        if local_rows.shape != (self.R, self.n_cols):
+            raise ShapeMismatch(f"local rows {tuple(local_rows.shape)} != {(self.R, self.n_cols)}")
+        self.handle.barrier(channel=0)
+        kernels.remap_routed(local_rows.reshape(-1), None, self.layout, self.peers, self.route)
+        self.handle.barrier(channel=0)
+        return self.out
 
 
 def fused_transpose_route(R: int, C: int, world: int, rank: int):
