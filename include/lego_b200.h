@@ -56,14 +56,16 @@ typedef enum {
     LEGO_PROG_BAND = 3,        /* remap: anti-diagonal band tiles through shared memory */
     LEGO_PROG_SCATTER = 4,     /* remap into an injective layout: dst[apply(x)] = src[x] */
     LEGO_PROG_STAGED = 5,      /* remap: per-block source box staged through smem      */
-    LEGO_PROG_NW = 6           /* Needleman-Wunsch wavefront over a LEGO tile layout   */
+    LEGO_PROG_NW = 6,          /* Needleman-Wunsch wavefront over a LEGO tile layout   */
+    LEGO_PROG_SOFTMAX = 7      /* row softmax with a LEGO thread/data layout           */
 } lego_program_kind;
 
 /* Program geometry.  Index-map programs: n = logical size, units = physical
  * size.  Remap programs: n = destination elements per matrix (source
  * elements for SCATTER), units = CTAs per matrix (grid.x; grid.y = batch).
  * NW programs: n = matrix side, units = tile rows H (= n for column strips),
- * reserved = 1 when tiles publish bottom rows (more than one tile row). */
+ * reserved = 1 when tiles publish bottom rows (more than one tile row).
+ * Softmax programs: n = row length (cols), units = rows the layout covers. */
 
 typedef struct {
     int32_t kind;          /* lego_program_kind                                  */
@@ -116,6 +118,12 @@ lego_status lego_inv_map(lego_program p, void *out, int32_t out_bytes, int64_t f
  * hit != 1 times.  Synchronises the stream. */
 lego_status lego_check_bijective(lego_program p, uint32_t *hist, int64_t *violations,
                                  void *stream);
+/* The same histogram, counting positions hit more than once: the
+ * injectivity proof of an injective-mode layout (layout.py:304-311), whose
+ * unhit positions are legal.  Run before a scatter through a user GenP the
+ * reference would only "trust". */
+lego_status lego_check_injective(lego_program p, uint32_t *hist, int64_t *violations,
+                                 void *stream);
 
 /* --- layout remap (the data movement the index maps describe) ------------- */
 /* For batch b < batch:  dst[b*dst_stride + f] = src[b*src_stride + g(f)]
@@ -135,6 +143,18 @@ lego_status lego_remap(lego_program p, const void *src, void *dst, int64_t batch
  * access when cols % 4 == 0 and both buffers are 16-byte aligned; any other
  * shape takes a scalar two-pass kernel (4-byte alignment). */
 lego_status lego_softmax_f32(const float *x, float *y, int64_t rows, int64_t cols, void *stream);
+
+/* The register-resident softmax through a program generated from the LEGO
+ * thread/data layout GroupBy([R], [cols/(4T)], [T], [4]).OrderBy(Row(R, cols))
+ * (kernels.softmax_program, LEGO_PROG_SOFTMAX; T = 256, cols % 4T == 0):
+ * the kernel reads and writes element (row, it, tid, v) at the layout's
+ * apply(row, it, tid, v).  cols must equal the program's, rows <= R,
+ * buffers 16-byte aligned. */
+lego_status lego_softmax_run(lego_program p, const float *x, float *y, int64_t rows, int64_t cols,
+                             void *stream);
+/* Test support: the float offsets the program's kernel accesses for the
+ * first `rows` rows, out[(row*ITS + it)*T + tid] (int64, -1 past the row). */
+lego_status lego_softmax_offsets(lego_program p, int64_t *out, int64_t rows, void *stream);
 
 /* Needleman-Wunsch score matrix: score is (n+1) x (n+1) int32, row-major;
  * sim is n x n; batch independent alignments back to back.
@@ -173,6 +193,14 @@ lego_status lego_nw_run(lego_program p, const int32_t *sim, int32_t *score, int6
  * for all exact shapes). */
 lego_status lego_gemm_bf16(const void *A, const void *B, void *C, int64_t M, int64_t N,
                            int64_t K, int64_t batch, int32_t raster, void *stream);
+
+/* Test support: the GEMM kernels' tile order, out[3t..3t+2] = (batch, m-block,
+ * n-block) of tile t < mtiles*ntiles*batch, from the same device function
+ * the kernels use (raster = G > 0: grouped raster of G m-blocks; 0:
+ * row-major).  The single-CTA kernel passes m-blocks of 128 rows and G; the
+ * CTA-pair kernel m-blocks of 256 rows and G / 2. */
+lego_status lego_gemm_raster(int32_t *out, int64_t mtiles, int64_t ntiles, int64_t batch, int32_t raster,
+                             void *stream);
 
 /* The four data-layout variants of the paper's LEGO matmul (Row vs Col
  * layouts of each operand): a_major / b_major = 0 keeps

@@ -17,7 +17,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblego_b200.so")
 SOURCES = ["lego_runtime.cu", "softmax.cu", "wavefront.cu", "gemm_tcgen05.cu"]
-DEPS = ["lego_common.h", "lego_index.cuh", "remap_kernels.cuh", "nw_kernels.cuh", "../../include/lego_b200.h"]
+DEPS = ["lego_common.h", "lego_index.cuh", "remap_kernels.cuh", "nw_kernels.cuh", "softmax_kernels.cuh", "../../include/lego_b200.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -184,6 +184,33 @@ struct Raster {
     }
 };
 
+// tile t -> (batch, m-block, n-block): the LEGO grouped raster (raster_mode =
+// G > 0) or row-major (0).  The only tile-order arithmetic of both GEMM
+// kernels; lego_gemm_raster dumps it for tests/test_gemm_raster.py, which
+// compares it with the LEGO layout's inverse map on the device.
+__device__ __forceinline__ void tile_coords(const Raster& ras, int raster_mode, int t, int& b, int& m, int& n) {
+    if (raster_mode) {
+        ras.coords(t, b, m, n);
+    } else {
+        b = t / ras.per_batch;
+        const int r = t - b * ras.per_batch;
+        m = r / ras.nb;
+        n = r - m * ras.nb;
+    }
+}
+
+__global__ void gemm_raster_dump(int* __restrict__ out, int mtiles, int ntiles, int batch, int raster_mode) {
+    const Raster ras{mtiles, ntiles, mtiles * ntiles, raster_mode > 0 ? raster_mode : 1};
+    const int total = ras.per_batch * batch;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        int b, m, n;
+        tile_coords(ras, raster_mode, t, b, m, n);
+        out[3 * t] = b;
+        out[3 * t + 1] = m;
+        out[3 * t + 2] = n;
+    }
+}
+
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                   __nv_bfloat16* __restrict__ C, int M, int N, int K, int batch, int raster_mode) {
@@ -235,8 +262,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
                 int b, mb, nb;
-                if (raster_mode) ras.coords(t, b, mb, nb);
-                else { b = t / ras.per_batch; int r = t - b * ras.per_batch; mb = r / ras.nb; nb = r - mb * ras.nb; }
+                tile_coords(ras, raster_mode, t, b, mb, nb);
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
@@ -283,8 +309,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         int it = 0;
         for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
             int b, mb, nb;
-            if (raster_mode) ras.coords(t, b, mb, nb);
-            else { b = t / ras.per_batch; int r = t - b * ras.per_batch; mb = r / ras.nb; nb = r - mb * ras.nb; }
+            tile_coords(ras, raster_mode, t, b, mb, nb);
             const int acc = it & 1;
             mbar_wait(&acc_full[acc], (it >> 1) & 1);
             tc_fence_after();
@@ -470,10 +495,7 @@ gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     const uint32_t full_leader = map_to_cta(smem_u32(full_bar), 0);
     const uint32_t acc_empty_leader = map_to_cta(smem_u32(acc_empty), 0);
 
-    auto coords = [&](int t, int& b, int& m, int& n) {
-        if (raster_mode) ras.coords(t, b, m, n);
-        else { b = t / ras.per_batch; int r = t - b * ras.per_batch; m = r / ras.nb; n = r - m * ras.nb; }
-    };
+    auto coords = [&](int t, int& b, int& m, int& n) { tile_coords(ras, raster_mode, t, b, m, n); };
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================
@@ -745,13 +767,9 @@ template <int NH, bool TA, bool TB>
 lego_status launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t M, int64_t N, int64_t K,
                         int64_t batch, int raster, int64_t pairs, void* stream) {
     using C_ = pair::Cfg<NH>;
-    static std::once_flag once;
-    static cudaError_t err = cudaSuccess;
-    std::call_once(once, [] {
-        err = cudaFuncSetAttribute(pair::gemm_bf16_tcgen05_pair<NH, TA, TB>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES);
-    });
-    LEGO_TRY(lego_cuda_check(err, "cudaFuncSetAttribute(gemm pair smem)"));
+    static std::atomic<unsigned long long> attr_set{0};
+    LEGO_TRY(lego_smem_optin(pair::gemm_bf16_tcgen05_pair<NH, TA, TB>, C_::SMEM_BYTES, attr_set,
+                             "cudaFuncSetAttribute(gemm pair smem)"));
     pair::gemm_bf16_tcgen05_pair<NH, TA, TB><<<(unsigned)(2 * pairs), C_::NUM_THREADS, C_::SMEM_BYTES,
                                                static_cast<cudaStream_t>(stream)>>>(
         ma, mb, static_cast<__nv_bfloat16*>(C), (int)M, (int)N, (int)K, (int)batch, raster);
@@ -819,12 +837,8 @@ lego_status gemm_impl(const void* A, const void* B, void* C, int64_t M, int64_t 
     CUtensorMap ma, mb;
     LEGO_TRY(make_map(&ma, A, M, K, batch, BM));
     LEGO_TRY(make_map(&mb, B, N, K, batch, BN));
-    static std::once_flag attr_once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(attr_once, [] {
-        attr_err = cudaFuncSetAttribute(gemm_bf16_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    });
-    LEGO_TRY(lego_cuda_check(attr_err, "cudaFuncSetAttribute(gemm smem)"));
+    static std::atomic<unsigned long long> attr_set{0};
+    LEGO_TRY(lego_smem_optin(gemm_bf16_tcgen05, SMEM_BYTES, attr_set, "cudaFuncSetAttribute(gemm smem)"));
     const int64_t tiles = (M / BM) * (N / BN) * batch;
     const int grid = (int)(tiles < sms ? tiles : sms);
     gemm_bf16_tcgen05<<<grid, NUM_THREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
@@ -833,6 +847,19 @@ lego_status gemm_impl(const void* A, const void* B, void* C, int64_t M, int64_t 
 }
 
 }  // namespace
+
+extern "C" lego_status lego_gemm_raster(int32_t* out, int64_t mtiles, int64_t ntiles, int64_t batch,
+                                        int32_t raster, void* stream) {
+    if (mtiles <= 0 || ntiles <= 0 || batch <= 0 || mtiles * ntiles * batch > INT32_MAX / 3)
+        return lego_fail(LEGO_E_SHAPE, "bad raster size");
+    if (raster < 0) return lego_fail(LEGO_E_ARG, "raster group must be >= 0");
+    if (!out) return lego_fail(LEGO_E_ARG, "null buffer");
+    const long long total = mtiles * ntiles * batch;
+    const unsigned grid = (unsigned)((total + 255) / 256 < 1024 ? (total + 255) / 256 : 1024);
+    gemm_raster_dump<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(out, (int)mtiles, (int)ntiles,
+                                                                           (int)batch, raster);
+    return lego_cuda_check(cudaGetLastError(), "raster dump");
+}
 
 extern "C" lego_status lego_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                                       int64_t batch, int32_t raster, void* stream) {

@@ -195,6 +195,7 @@ struct lego_program_s {
     CUfunction_t apply32 = nullptr, apply64 = nullptr, inv32 = nullptr, inv64 = nullptr;
     CUfunction_t hist = nullptr, hist_check = nullptr;
     CUfunction_t nw_tiles = nullptr, nw_borders = nullptr;
+    CUfunction_t sm_rows = nullptr, sm_offsets = nullptr;
 };
 
 extern "C" lego_status lego_program_load(const void* cubin, size_t cubin_len,
@@ -224,6 +225,14 @@ extern "C" lego_status lego_program_load(const void* cubin, size_t cubin_len,
             g_drv.unload(p->mod);
             delete p;
             return lego_fail(LEGO_E_ARG, "index-map program lacks its kernels");
+        }
+    } else if (info->kind == LEGO_PROG_SOFTMAX) {
+        bool ok = !g_drv.get_fn(&p->sm_rows, p->mod, "lego_softmax_rows") &&
+                  !g_drv.get_fn(&p->sm_offsets, p->mod, "lego_softmax_offsets");
+        if (!ok) {
+            g_drv.unload(p->mod);
+            delete p;
+            return lego_fail(LEGO_E_ARG, "softmax program lacks its kernels");
         }
     } else if (info->kind == LEGO_PROG_NW) {
         if (info->smem_bytes != lego_nw_smem_bytes()) {
@@ -307,8 +316,8 @@ extern "C" lego_status lego_inv_map(lego_program p, void* out, int32_t out_bytes
     return index_map(p, 1, out, out_bytes, first, count, stream);
 }
 
-extern "C" lego_status lego_check_bijective(lego_program p, uint32_t* hist, int64_t* violations,
-                                            void* stream) {
+static lego_status check_hits(lego_program p, uint32_t* hist, int64_t* violations, int at_most_once,
+                              void* stream) {
     if (!p || p->info.kind != LEGO_PROG_INDEX_MAP)
         return lego_fail(LEGO_E_ARG, "program is not an index-map program");
     if (!hist || !violations) return lego_fail(LEGO_E_ARG, "null argument");
@@ -323,7 +332,7 @@ extern "C" lego_status lego_check_bijective(lego_program p, uint32_t* hist, int6
     cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)n_out, st);
     void* a1[] = {&hist, &count, &n_out, &bad};
     if ((s = launch(p->hist, map_grid(count), 1, 256, 0, stream, a1))) return s;
-    void* a2[] = {&hist, &n_out, &bad};
+    void* a2[] = {&hist, &n_out, &bad, &at_most_once};
     if ((s = launch(p->hist_check, map_grid(n_out), 1, 256, 0, stream, a2))) return s;
     unsigned long long host = 0;
     cudaMemcpyAsync(&host, bad, sizeof host, cudaMemcpyDeviceToHost, st);
@@ -331,6 +340,41 @@ extern "C" lego_status lego_check_bijective(lego_program p, uint32_t* hist, int6
     if ((s = lego_cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return s;
     *violations = (int64_t)host;
     return LEGO_OK;
+}
+
+extern "C" lego_status lego_check_bijective(lego_program p, uint32_t* hist, int64_t* violations,
+                                            void* stream) {
+    return check_hits(p, hist, violations, 0, stream);
+}
+
+extern "C" lego_status lego_check_injective(lego_program p, uint32_t* hist, int64_t* violations,
+                                            void* stream) {
+    return check_hits(p, hist, violations, 1, stream);
+}
+
+extern "C" lego_status lego_softmax_run(lego_program p, const float* x, float* y, int64_t rows, int64_t cols,
+                                        void* stream) {
+    if (!p || p->info.kind != LEGO_PROG_SOFTMAX) return lego_fail(LEGO_E_ARG, "program is not a softmax program");
+    if (cols != p->info.n)
+        return lego_fail(LEGO_E_SHAPE, "program was built for %lld columns, called with %lld",
+                         (long long)p->info.n, (long long)cols);
+    if (rows < 0 || rows > p->info.units || rows > 0x7fffffffLL)
+        return lego_fail(LEGO_E_SHAPE, "rows %lld outside the program's layout (%lld)", (long long)rows,
+                         (long long)p->info.units);
+    if (rows == 0) return LEGO_OK;
+    if (!x || !y) return lego_fail(LEGO_E_ARG, "null buffer");
+    if (((uintptr_t)x | (uintptr_t)y) & 15) return lego_fail(LEGO_E_ARG, "buffers must be 16-byte aligned");
+    void* args[] = {&x, &y};
+    return launch(p->sm_rows, (unsigned)rows, 1, (unsigned)p->info.block, 0, stream, args);
+}
+
+extern "C" lego_status lego_softmax_offsets(lego_program p, int64_t* out, int64_t rows, void* stream) {
+    if (!p || p->info.kind != LEGO_PROG_SOFTMAX) return lego_fail(LEGO_E_ARG, "program is not a softmax program");
+    if (rows < 0 || rows > p->info.units || rows > 0x7fffffffLL) return lego_fail(LEGO_E_SHAPE, "bad rows");
+    if (rows == 0) return LEGO_OK;
+    if (!out) return lego_fail(LEGO_E_ARG, "null buffer");
+    void* args[] = {&out};
+    return launch(p->sm_offsets, (unsigned)rows, 1, (unsigned)p->info.block, 0, stream, args);
 }
 
 extern "C" lego_status lego_nw_run(lego_program p, const int32_t* sim, int32_t* score, int64_t n,

@@ -401,6 +401,7 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
         }
 #else
         tl.top_in = tl.top_out = nullptr;
+        (void)top_s;
 #endif
         const int rows_total = (tl.nblocks + DRAIN) * BLK;
 

@@ -157,12 +157,14 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_hist(unsigned int* hist, long long 
         else if (r != -1) atomicAdd(bad, 1ull);
     }
 }
+// violations: positions not hit exactly once (bijective), or hit more than
+// once (at_most_once: injective-mode layouts leave positions unhit)
 LEGO_GLOBAL void __launch_bounds__(256) lego_hist_check(const unsigned int* hist, long long n,
-                                                        unsigned long long* bad) {
+                                                        unsigned long long* bad, int at_most_once) {
     long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
     unsigned long long local = 0;
-    for (; k < n; k += stride) local += (hist[k] != 1u);
+    for (; k < n; k += stride) local += at_most_once ? (hist[k] > 1u) : (hist[k] != 1u);
     for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(bad, local);
 }

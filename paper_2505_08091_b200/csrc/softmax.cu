@@ -1,94 +1,30 @@
-// softmax.cu -- row softmax, fp32, one CTA per row (BASELINE.json config 3).
-//
-// Thread/data layout is the LEGO layout
-//     GroupBy([rows], [cols/(4T)], [T], [4]).OrderBy(Row(rows, cols))
-// i.e. element (row, it, tid, v) lives at row*cols + it*4T + tid*4 + v
-// (tests/test_softmax_layout.py derives this offset with apply_symbolic):
-// every warp access is a coalesced float4, and a row is held in registers,
-// so HBM sees one read and one write per element.  When a row does not fit
-// the register budget the kernel streams it twice (online max/sum, then the
-// normalised write).
+// softmax.cu -- row softmax, fp32, one CTA per row (BASELINE.json config 3):
+// the library's built-in kernels.  The register-resident kernel is the
+// template of softmax_kernels.cuh with the layout's offset written for a
+// runtime row length; kernels.softmax runs the LEGO-generated program of
+// the same template (offsets from GroupBy([rows],[cols/4T],[T],[4])
+// .OrderBy(Row(rows, cols)), tests/test_softmax_layout.py) whenever the row
+// length is a whole number of 4T-float passes.  Long rows stream twice
+// (online max/sum, then the normalised write); ragged rows take a scalar
+// kernel.
 #include <cuda_runtime.h>
 
 #include "lego_common.h"
 
+#define SM_GLOBAL static __global__
+#include "softmax_kernels.cuh"
+
 namespace {
 
-constexpr int kThreads = 256;
+using smk::block_reduce;
+using smk::kLog2e;
+using smk::kThreads;
+using smk::st_stream;
 
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// block-wide reduction through shared memory (8 warps)
-template <bool IsMax>
-__device__ __forceinline__ float block_reduce(float v, float* red) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    v = IsMax ? warp_max(v) : warp_sum(v);
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    float r = lane < (kThreads / 32) ? red[lane] : (IsMax ? -INFINITY : 0.f);
-    r = IsMax ? warp_max(r) : warp_sum(r);
-    __syncthreads();
-    return r;
-}
-
-__device__ __forceinline__ float4 ld_stream(const float4* p) {
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ void st_stream(float4* p, float4 v) {
-    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
-                 "f"(v.w) : "memory");
-}
-
-constexpr float kLog2e = 1.4426950408889634f;
-
-// IT = float4 vectors per thread: the whole row lives in registers
 template <int IT>
 __global__ void __launch_bounds__(kThreads) softmax_rows_reg(const float* __restrict__ x,
                                                              float* __restrict__ y, long long cols) {
-    __shared__ float red[kThreads / 32];
-    const long long row = blockIdx.x;
-    const float4* xr = reinterpret_cast<const float4*>(x + row * cols);
-    float4* yr = reinterpret_cast<float4*>(y + row * cols);
-    const int nvec = (int)(cols >> 2);
-    float4 v[IT];
-    float m = -INFINITY;
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-        const int k = it * kThreads + threadIdx.x;          // offset it*4T + tid*4 (in floats)
-        v[it] = k < nvec ? ld_stream(xr + k) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-        m = fmaxf(m, fmaxf(fmaxf(v[it].x, v[it].y), fmaxf(v[it].z, v[it].w)));
-    }
-    m = block_reduce<true>(m, red);
-    const float mb = m * kLog2e;
-    float s = 0.f;
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-        v[it].x = exp2f(fmaf(v[it].x, kLog2e, -mb));
-        v[it].y = exp2f(fmaf(v[it].y, kLog2e, -mb));
-        v[it].z = exp2f(fmaf(v[it].z, kLog2e, -mb));
-        v[it].w = exp2f(fmaf(v[it].w, kLog2e, -mb));
-        s += (v[it].x + v[it].y) + (v[it].z + v[it].w);
-    }
-    s = block_reduce<false>(s, red);
-    const float inv = 1.f / s;
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-        const int k = it * kThreads + threadIdx.x;
-        if (k < nvec)
-            st_stream(yr + k, make_float4(v[it].x * inv, v[it].y * inv, v[it].z * inv, v[it].w * inv));
-    }
+    smk::softmax_reg_body<IT>(x, y, cols);
 }
 
 // long rows: online (max, sum) pass, then a normalising pass

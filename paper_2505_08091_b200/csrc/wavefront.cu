@@ -115,16 +115,8 @@ extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n
     if (batch == 0) return LEGO_OK;
     lego_nw_borders<<<pl.border_ctas, 256, 0, st>>>(score, n, penalty, batch);
     if (n == 0) return lego_cuda_check(cudaGetLastError(), "nw borders");
-    // the >48 KiB dynamic shared memory opt-in is a per-device function attribute
     static std::atomic<unsigned long long> attr_set{0};
-    int dev = 0;
-    LEGO_TRY(lego_cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
-    const unsigned long long bit = 1ull << (dev & 63);
-    if (!(attr_set.load() & bit)) {
-        LEGO_TRY(lego_cuda_check(cudaFuncSetAttribute(lego_nw_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                      nwk::SMEM_BYTES), "cudaFuncSetAttribute(nw)"));
-        attr_set.fetch_or(bit);
-    }
+    LEGO_TRY(lego_smem_optin(lego_nw_tiles, nwk::SMEM_BYTES, attr_set, "cudaFuncSetAttribute(nw)"));
 #ifdef LEGO_NW_DEBUG
     {
         void* trace = nullptr;

@@ -1,7 +1,11 @@
 """The GEMM's data, thread and shared-memory layouts written as LEGO layouts.
 
 * ``raster_layout(mb, nb, g)`` -- the CTA tile raster walked by
-  ``csrc/gemm_tcgen05.cu`` (``Raster::coords`` evaluates its inverse).
+  ``csrc/gemm_tcgen05.cu`` when g divides mb (``tile_coords`` evaluates its
+  inverse); ``grouped_raster_perm(mb, nb, g)`` -- the same order for any mb,
+  a user-defined GenP over the (m-block, n-block) grid whose last group
+  holds the mb % g remaining m-blocks (tests/test_gemm_raster.py compares
+  both with the device's tile order).
 * ``sw128_perm()`` -- the 128-byte shared-memory swizzle that TMA
   (``CU_TENSOR_MAP_SWIZZLE_128B``) writes and the UMMA descriptors
   (layout type 2) read: inside a 1024-byte atom of 8 rows x 8 16-byte chunks,
@@ -16,8 +20,9 @@
 
 from __future__ import annotations
 
-from .layout import GenP, GroupBy, OrderBy, PermFn, RegP
 from .dsl import parse_layout
+from .expr import Select, lt
+from .layout import GenP, GroupBy, OrderBy, PermFn, RegP
 
 
 def _xor3(a, b):
@@ -58,3 +63,40 @@ def kmajor_smem_layout(rows: int, k: int = 64) -> GroupBy:
 def raster_layout(mb: int, nb: int, g: int) -> GroupBy:
     """Tile raster: tile t -> (group, n-block, m within group), m fastest."""
     return parse_layout(f"GroupBy([{mb // g},{nb},{g}]).OrderBy(Row({mb // g},{nb},{g}))")
+
+
+def grouped_raster_perm(mb: int, nb: int, g: int) -> GenP:
+    """Tile (m, n) -> rank t of the grouped raster: groups of g m-blocks, each
+    walked n-major with m fastest; a last group of mb % g m-blocks."""
+    full = (mb // g) * g
+    tail = mb - full
+
+    def fwd(idx):
+        m, n = idx
+        if m < full:
+            return ((m // g) * nb + n) * g + m % g
+        return full * nb + n * tail + (m - full)
+
+    def fwd_sym(idx):
+        m, n = idx
+        t_tail = (m - full) + n * tail + full * nb
+        return Select(lt(m, full), ((m // g) * nb + n) * g + m % g, t_tail) if tail else \
+            ((m // g) * nb + n) * g + m % g
+
+    def inv(t):
+        if t < full * nb:
+            grp, rem = divmod(t, g * nb)
+            return grp * g + rem % g, rem // g
+        rem = t - full * nb
+        return full + rem % tail, rem // tail
+
+    def inv_sym(t):
+        rem = t % (g * nb)
+        m_full, n_full = (t // (g * nb)) * g + rem % g, rem // g
+        if not tail:
+            return m_full, n_full
+        r2 = t - full * nb
+        head = lt(t, full * nb)
+        return Select(head, m_full, full + r2 % tail), Select(head, n_full, r2 // tail)
+
+    return GenP((mb, nb), PermFn(fwd, fwd_sym), PermFn(inv, inv_sym), name=None)

@@ -36,8 +36,6 @@ from .simplify import _lin_of
 
 CSRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc")
 _TEXT: Dict[str, str] = {}
-_PROGRAMS: Dict[tuple, runtime.Program] = {}
-_PLOCK = threading.Lock()
 
 # kernel launches issued through this module since import (for bench.py's
 # gpu_launches count; the driver cross-checks with the loaded .so list)
@@ -68,16 +66,59 @@ def _layout_key(layout) -> tuple:
 # program builders
 # ---------------------------------------------------------------------------
 
-def _program(key, builder):
-    prog = _PROGRAMS.get(key)
-    if prog is None:
-        with _PLOCK:
-            prog = _PROGRAMS.get(key)
-            if prog is None:
-                source, info = builder()
-                prog = runtime.Program(runtime.compile_cubin(source), info, source)
-                _PROGRAMS[key] = prog
-    return prog
+class _ProgramCache:
+    """Loaded programs, per device.  Two levels: (layout key, device) ->
+    program (an LRU: layouts holding user GenPs compare by closure identity,
+    so every fresh parse is a new key) and (source SHA-256, device) ->
+    program, so re-planning an equal layout reuses the loaded module instead
+    of loading another.  A program is published only once complete."""
+
+    def __init__(self, limit: int = 256):
+        from collections import OrderedDict
+        self.limit = limit
+        self.by_key = OrderedDict()
+        self.by_source: Dict[tuple, runtime.Program] = {}
+        self.lock = threading.Lock()
+
+    def get(self, key, builder, device: int):
+        k = key + (device,)
+        with self.lock:
+            prog = self.by_key.get(k)
+            if prog is not None:
+                self.by_key.move_to_end(k)
+                return prog
+        source, info, extra = builder()
+        import hashlib
+        sk = (hashlib.sha256(source.encode()).hexdigest(), device)
+        with self.lock:
+            prog = self.by_source.get(sk)
+        if prog is None:
+            import torch
+            cubin = runtime.compile_cubin(source)
+            with torch.cuda.device(device):
+                prog = runtime.Program(cubin, info, source)
+            for name, value in (extra or {}).items():
+                setattr(prog, name, value)
+        with self.lock:
+            prog = self.by_source.setdefault(sk, prog)
+            self.by_key[k] = prog
+            self.by_key.move_to_end(k)
+            while len(self.by_key) > self.limit:
+                _old_key, old = self.by_key.popitem(last=False)
+                if not any(p is old for p in self.by_key.values()):
+                    self.by_source = {kk: pp for kk, pp in self.by_source.items() if pp is not old}
+        return prog
+
+
+_CACHE = _ProgramCache()
+
+
+def _program(key, builder, device: int):
+    """builder() -> (source, info) or (source, info, {attr: value})."""
+    def build():
+        got = builder()
+        return got if len(got) == 3 else (got[0], got[1], None)
+    return _CACHE.get(key, build, device)
 
 
 def index_map_source(layout) -> Tuple[str, runtime.ProgramInfo]:
@@ -424,26 +465,24 @@ def _scatter_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
                      f"scatter into an injective layout, {n_dst} positions")
 
 
-def _remap_program(src_layout, dst_layout, elem_bytes, route=None):
+def _remap_program(src_layout, dst_layout, elem_bytes, device: int, route=None):
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes,
            None if route is None else ("route", route.world, route.key), TRANSPOSE_VARIANT,
            BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB,
            BAND_ROWS, BAND_DIAGS, BAND_WARPS, TRANSPOSE_WARPS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE,
            staging.BOX_BULK, staging.BOX_THREADS)
-    plans = []
 
     def build():
-        plans.append(plan_remap(src_layout, dst_layout, elem_bytes, route))
-        return plans[0].source, plans[0].info
+        plan = plan_remap(src_layout, dst_layout, elem_bytes, route)
+        # the sizes it was planned for travel with the program (set before publication)
+        return plan.source, plan.info, {"n_dst": plan.n_dst, "n_src": plan.n_src, "kind": plan.kind,
+                                        "gated": _needs_bijectivity_gate(src_layout, dst_layout, plan)}
 
-    prog = _program(key, build)
-    if plans:                      # freshly built: remember the sizes it was planned for
-        prog.n_dst, prog.n_src = plans[0].n_dst, plans[0].n_src
-    return prog
+    return _program(key, build, device)
 
 
-def _map_program(layout):
-    return _program(("map", _layout_key(layout)), lambda: index_map_source(layout))
+def _map_program(layout, device: int):
+    return _program(("map", _layout_key(layout)), lambda: index_map_source(layout), device)
 
 
 # ---------------------------------------------------------------------------
@@ -459,7 +498,82 @@ def _device(device):
     torch = _torch()
     if device is None:
         device = torch.device("cuda", torch.cuda.current_device())
-    return torch.device(device)
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise ShapeMismatch(f"the backend runs on CUDA devices only, got {device}")
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    return device
+
+
+def _check_out(out, shape, dtype, device, what, min_numel=None):
+    """Caller-provided outputs go to the C ABI as bare pointers: check them."""
+    if dtype is not None and out.dtype not in (dtype if isinstance(dtype, tuple) else (dtype,)):
+        raise ShapeMismatch(f"{what}: out has dtype {out.dtype}, expected {dtype}")
+    if out.device != device:
+        raise ShapeMismatch(f"{what}: out is on {out.device}, expected {device}")
+    if not out.is_contiguous():
+        raise ShapeMismatch(f"{what}: out must be contiguous")
+    if shape is not None and tuple(out.shape) != tuple(shape):
+        raise ShapeMismatch(f"{what}: out has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    if min_numel is not None and out.numel() < min_numel:
+        raise ShapeMismatch(f"{what}: out holds {out.numel()} elements, needs {min_numel}")
+
+
+# reference validate() enumerates GenPs only up to this many points and
+# "trusts" larger ones (pkg/src/lego/layout.py:718-719)
+TRUST_BOUND = 4096
+_BUILTIN_FACTORIES = ("identity_perm", "reverse_perm", "antidiag_perm")
+
+
+def _builtin_genp(p) -> bool:
+    """A GenP made by this package's built-in factories (bijective by
+    construction); user GenPs -- even ones named like a built-in -- are not."""
+    from . import layout as _layout
+    fn = getattr(p.fwd, "concrete", None)
+    return (getattr(fn, "__module__", None) == _layout.__name__
+            and getattr(fn, "__qualname__", "").split(".")[0] in _BUILTIN_FACTORIES)
+
+
+def _untrusted_genps(layout) -> bool:
+    if layout is None:
+        return False
+    from .layout import GenP
+    g = lower._group(layout)
+    return any(isinstance(p, GenP) and p.size > TRUST_BOUND and not _builtin_genp(p)
+               for stage in g.orders for p in stage.perms)
+
+
+def _needs_bijectivity_gate(src_layout, dst_layout, plan):
+    """Layouts to prove on the device before the first launch of a plan that
+    *stores* through positions computed from a user GenP the reference only
+    trusts (a non-injective GenP makes a scatter
+    race).  Gathers enumerate the destination, so each element is written
+    once whatever the map.  Returns [(layout, 'bijective'|'injective')]."""
+    gates = []
+    if plan.kind == runtime.KIND_SCATTER and _untrusted_genps(dst_layout):
+        gates.append((dst_layout, "injective"))
+    elif plan.kind == runtime.KIND_STAGED and plan.detail.startswith("source blocks"):
+        gates += [(side, "bijective") for side in (src_layout, dst_layout) if _untrusted_genps(side)]
+    elif plan.kind == runtime.KIND_BAND and plan.detail.endswith("scatter") and _untrusted_genps(dst_layout):
+        gates.append((dst_layout, "bijective"))
+    return gates
+
+
+def _run_gates(prog, device):
+    gates = getattr(prog, "gated", None)
+    if not gates:
+        return
+    for layout, mode in gates:
+        if mode == "injective":
+            ok = check_injective(layout, device=device)
+        else:
+            ok = check_bijective(layout, device=device)
+        if not ok:
+            raise BijectivityViolation(f"layout {layout!r} is not {mode} on the device; a store through it "
+                                       "would race (the reference only trusts GenPs above "
+                                       f"{TRUST_BOUND} points)")
+    prog.gated = []            # proven once per program
 
 
 def apply_map(layout, *, dtype=None, device=None, first: int = 0, count: Optional[int] = None,
@@ -469,48 +583,81 @@ def apply_map(layout, *, dtype=None, device=None, first: int = 0, count: Optiona
     torch = _torch()
     n = lower.logical_size(layout)
     count = n - first if count is None else count
-    prog = _map_program(layout)
+    if first < 0 or count < 0 or first + count > n:
+        from .errors import OutOfBounds
+        raise OutOfBounds(f"range [{first}, {first + count}) outside the logical space of {n}")
+    dev = _device(out.device if out is not None else device)
+    prog = _map_program(layout, dev.index)
     if out is None:
         dtype = dtype or (torch.int32 if lower.physical_size(layout) < 2 ** 31 else torch.int64)
-        out = torch.empty(count, dtype=dtype, device=_device(device))
-    runtime.check(runtime.lib().lego_apply_map(prog.handle, out.data_ptr(), out.element_size(),
-                                               first, count, runtime.stream_handle(stream)),
-                  "lego_apply_map")
+        out = torch.empty(count, dtype=dtype, device=dev)
+    else:
+        _check_out(out, None, (torch.int32, torch.int64), dev, "apply_map", min_numel=count)
+    with torch.cuda.device(dev):
+        runtime.check(runtime.lib().lego_apply_map(prog.handle, out.data_ptr(), out.element_size(),
+                                                   first, count, runtime.stream_handle(stream)),
+                      "lego_apply_map")
     LAUNCHES[0] += 1
     return out
 
 
 def inv_map(layout, *, dtype=None, device=None, first: int = 0, count: Optional[int] = None,
             out=None, stream=None):
-    """``out[k] = canon_flatten(dims, layout.inv(first + k))`` on the GPU."""
+    """``out[k] = canon_flatten(dims, layout.inv(first + k))`` on the GPU.
+    Injective-mode layouts export ``apply`` only and raise, as the reference's
+    ``GroupBy.inv`` does (layout.py:321-322)."""
     torch = _torch()
+    if getattr(lower._group(layout), "injective", False):
+        from .errors import LegoError
+        raise LegoError("injective layout exports apply only, not inv")
     n = lower.physical_size(layout)
     count = n - first if count is None else count
-    prog = _map_program(layout)
+    if first < 0 or count < 0 or first + count > n:
+        from .errors import OutOfBounds
+        raise OutOfBounds(f"range [{first}, {first + count}) outside the physical space of {n}")
+    dev = _device(out.device if out is not None else device)
+    prog = _map_program(layout, dev.index)
     if out is None:
         dtype = dtype or (torch.int32 if lower.logical_size(layout) < 2 ** 31 else torch.int64)
-        out = torch.empty(count, dtype=dtype, device=_device(device))
-    runtime.check(runtime.lib().lego_inv_map(prog.handle, out.data_ptr(), out.element_size(),
-                                             first, count, runtime.stream_handle(stream)),
-                  "lego_inv_map")
+        out = torch.empty(count, dtype=dtype, device=dev)
+    else:
+        _check_out(out, None, (torch.int32, torch.int64), dev, "inv_map", min_numel=count)
+    with torch.cuda.device(dev):
+        runtime.check(runtime.lib().lego_inv_map(prog.handle, out.data_ptr(), out.element_size(),
+                                                 first, count, runtime.stream_handle(stream)),
+                      "lego_inv_map")
     LAUNCHES[0] += 1
     return out
 
 
+def _check_hits(layout, fn_name, device, stream):
+    torch = _torch()
+    dev = _device(device)
+    prog = _map_program(layout, dev.index)
+    hist = torch.empty(lower.physical_size(layout), dtype=torch.int32, device=dev)
+    bad = runtime.I64()
+    with torch.cuda.device(dev):
+        runtime.check(getattr(runtime.lib(), fn_name)(prog.handle, hist.data_ptr(), ctypes.byref(bad),
+                                                      runtime.stream_handle(stream)), fn_name)
+    LAUNCHES[0] += 2
+    return bad.value
+
+
 def check_bijective(layout, *, device=None, stream=None, raise_on_failure: bool = False) -> bool:
     """Device-side proof that ``apply`` hits every position exactly once."""
-    torch = _torch()
-    prog = _map_program(layout)
-    hist = torch.empty(lower.physical_size(layout), dtype=torch.int32, device=_device(device))
-    bad = runtime.I64()
-    runtime.check(runtime.lib().lego_check_bijective(prog.handle, hist.data_ptr(), ctypes.byref(bad),
-                                                     runtime.stream_handle(stream)),
-                  "lego_check_bijective")
-    LAUNCHES[0] += 2
-    ok = bad.value == 0
-    if not ok and raise_on_failure:
-        raise BijectivityViolation(f"{bad.value} positions are not hit exactly once")
-    return ok
+    bad = _check_hits(layout, "lego_check_bijective", device, stream)
+    if bad and raise_on_failure:
+        raise BijectivityViolation(f"{bad} positions are not hit exactly once")
+    return bad == 0
+
+
+def check_injective(layout, *, device=None, stream=None, raise_on_failure: bool = False) -> bool:
+    """Device-side proof that ``apply`` hits no position twice (injective-mode
+    layouts may leave positions unhit)."""
+    bad = _check_hits(layout, "lego_check_injective", device, stream)
+    if bad and raise_on_failure:
+        raise BijectivityViolation(f"{bad} positions are hit more than once")
+    return bad == 0
 
 
 def remap_plan(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
@@ -527,7 +674,8 @@ def remap(src, src_layout=None, dst_layout=None, *, out=None, stream=None):
         raise ShapeMismatch("remap takes a CUDA tensor (no CPU path)")
     elem = src.element_size()
     lower.check_pair(src_layout, dst_layout)
-    prog = _remap_program(src_layout, dst_layout, elem)
+    dev = src.device
+    prog = _remap_program(src_layout, dst_layout, elem, dev.index)
     f_dst, n_src = prog.n_dst, prog.n_src
     if src.numel() % n_src:
         raise ShapeMismatch(f"source of {src.numel()} elements is not a batch of layouts of "
@@ -537,18 +685,22 @@ def remap(src, src_layout=None, dst_layout=None, *, out=None, stream=None):
     batch_shape = tuple(src.shape[:-1]) if src.dim() and src.shape[-1] == n_src else (batch,)
     if out is None:
         alloc = torch.zeros if prog.info.kind == runtime.KIND_SCATTER else torch.empty
-        out = alloc(*batch_shape, f_dst, dtype=src.dtype, device=src.device)
-    st = runtime.stream_handle(stream)
-    done = 0
-    while done < batch or (batch == 0 and done == 0):
-        if batch == 0:
-            break
-        b = min(65535, batch - done)
-        runtime.check(runtime.lib().lego_remap(
-            prog.handle, src.data_ptr() + done * n_src * elem, out.data_ptr() + done * f_dst * elem,
-            b, n_src, f_dst, st), "lego_remap")
-        LAUNCHES[0] += 1
-        done += b
+        out = alloc(*batch_shape, f_dst, dtype=src.dtype, device=dev)
+    else:
+        _check_out(out, None, src.dtype, dev, "remap", min_numel=batch * f_dst)
+    if batch == 0:
+        return out
+    _run_gates(prog, dev)
+    with torch.cuda.device(dev):
+        st = runtime.stream_handle(stream)
+        done = 0
+        while done < batch:
+            b = min(65535, batch - done)
+            runtime.check(runtime.lib().lego_remap(
+                prog.handle, src.data_ptr() + done * n_src * elem, out.data_ptr() + done * f_dst * elem,
+                b, n_src, f_dst, st), "lego_remap")
+            LAUNCHES[0] += 1
+            done += b
     return out
 
 
@@ -569,13 +721,15 @@ def remap_routed(src, src_layout, dst_layout, peers, route: Route, *, stream=Non
         raise ShapeMismatch("the peer table must live on the source's device")
     elem = src.element_size()
     lower.check_pair(src_layout, dst_layout)
-    prog = _remap_program(src_layout, dst_layout, elem, route)
+    dev = src.device
+    prog = _remap_program(src_layout, dst_layout, elem, dev.index, route)
     if src.numel() != prog.n_src:
         raise ShapeMismatch(f"routed remap moves one layout of {prog.n_src} elements, got {src.numel()}")
     src = src.contiguous()
-    runtime.check(runtime.lib().lego_remap(prog.handle, src.data_ptr(), peers.data_ptr(), 1,
-                                           prog.n_src, prog.n_dst, runtime.stream_handle(stream)),
-                  "lego_remap")
+    with torch.cuda.device(dev):
+        runtime.check(runtime.lib().lego_remap(prog.handle, src.data_ptr(), peers.data_ptr(), 1,
+                                               prog.n_src, prog.n_dst, runtime.stream_handle(stream)),
+                      "lego_remap")
     LAUNCHES[0] += 1
 
 
@@ -593,17 +747,79 @@ def scatter(src, layout, **kw):
 # fixed kernels
 # ---------------------------------------------------------------------------
 
+SOFTMAX_THREADS = 256          # T of the thread layout (softmax_kernels.cuh kThreads)
+SOFTMAX_MAX_ITS = 16           # float4 vectors per thread held in registers
+
+
+def softmax_layout(cols: int, rows: Optional[int] = None):
+    """The softmax thread/data layout of the paper:
+    ``GroupBy([rows], [cols/(4T)], [T], [4]).OrderBy(Row(rows, cols))`` --
+    element (row, it, tid, v) of the thread decomposition lives at its
+    ``apply``.  ``rows`` defaults to the largest row count a program serves
+    (2^36 elements), so one program covers every batch of rows."""
+    from .layout import GroupBy, row
+    t4 = 4 * SOFTMAX_THREADS
+    if cols % t4:
+        raise ShapeMismatch(f"the register softmax layout needs cols % {t4} == 0, got {cols}")
+    rows = rows if rows is not None else max(1, (1 << 36) // cols)
+    return GroupBy([rows], [cols // t4], [SOFTMAX_THREADS], [4]).order_by(row(rows, cols))
+
+
+def softmax_source(cols: int):
+    """NVRTC source of the register softmax with its offsets generated from
+    :func:`softmax_layout` (gen::vec_of = apply(row, it, tid, 0) / 4)."""
+    lay = softmax_layout(cols)
+    rows = lay.dims[0]
+    its = cols // (4 * SOFTMAX_THREADS)
+    r = Var("row", VarRange(0, rows))
+    it = Var("it", VarRange(0, its))
+    tid = Var("tid", VarRange(0, SOFTMAX_THREADS))
+    pos = lower.apply_flat(lay, lower.as_expr(((r * its + it) * SOFTMAX_THREADS + tid) * 4))
+    vec = lower.simplify(lower.as_expr(lower.simplify(lower.as_expr(pos)) // 4))
+    body = codegen.constant("COLS", cols) + codegen.constant("ITS", its)
+    body += codegen.generate("vec_of", [r, it, tid], {"k": vec}).source
+    src = ("#define SM_GEN 1\n" + _text("lego_index.cuh").replace("#pragma once", "") + "\nnamespace gen {\n"
+           + body + "}\n" + _text("softmax_kernels.cuh").replace("#pragma once", ""))
+    info = runtime.ProgramInfo(kind=runtime.KIND_SOFTMAX, elem_bytes=4, n=cols, units=rows, unit_threads=1,
+                               block=SOFTMAX_THREADS, smem_bytes=0)
+    return src, info
+
+
+def softmax_program(cols: int, device=None):
+    dev = _device(device)
+    return _program(("softmax", cols), lambda: softmax_source(cols), dev.index)
+
+
+def softmax_generated(cols: int) -> bool:
+    """Whether rows of this length take the LEGO-generated program."""
+    t4 = 4 * SOFTMAX_THREADS
+    return cols > 0 and cols % t4 == 0 and cols // t4 <= SOFTMAX_MAX_ITS
+
+
 def softmax(x, *, out=None, stream=None):
-    """Row softmax over the last dim of a contiguous fp32 CUDA tensor."""
+    """Row softmax over the last dim of a contiguous fp32 CUDA tensor.  Rows
+    of a whole number of 4T-float passes (up to 16) run the program generated
+    from :func:`softmax_layout`; other lengths the library's built-in kernels."""
     torch = _torch()
-    if x.dtype != torch.float32 or not x.is_cuda:
+    if x.dtype != torch.float32 or not x.is_cuda or x.dim() == 0:
         raise ShapeMismatch("softmax takes a CUDA float32 tensor")
     x = x.contiguous()
     cols = x.shape[-1]
     rows = x.numel() // cols if cols else 0
-    out = torch.empty_like(x) if out is None else out
-    runtime.check(runtime.lib().lego_softmax_f32(x.data_ptr(), out.data_ptr(), rows, cols,
-                                                 runtime.stream_handle(stream)), "lego_softmax_f32")
+    if out is None:
+        out = torch.empty_like(x)
+    else:
+        _check_out(out, tuple(x.shape), torch.float32, x.device, "softmax")
+    with torch.cuda.device(x.device):
+        st = runtime.stream_handle(stream)
+        aligned = (x.data_ptr() | out.data_ptr()) % 16 == 0
+        if rows and softmax_generated(cols) and aligned and rows <= (1 << 36) // cols:
+            prog = softmax_program(cols, x.device)
+            runtime.check(runtime.lib().lego_softmax_run(prog.handle, x.data_ptr(), out.data_ptr(), rows, cols,
+                                                         st), "lego_softmax_run")
+        else:
+            runtime.check(runtime.lib().lego_softmax_f32(x.data_ptr(), out.data_ptr(), rows, cols, st),
+                          "lego_softmax_f32")
     LAUNCHES[0] += 1
     return out
 
@@ -636,22 +852,10 @@ def nw_score(sim, penalty: int, *, layout=None, out=None, stream=None):
         else:
             from . import nw
             prog = nw.nw_program(layout, n, device=sim.device)
-            runtime.check(runtime.lib().lego_nw_run(prog.prog.handle, sim.data_ptr(), out.data_ptr(), n,
+            runtime.check(runtime.lib().lego_nw_run(prog.handle, sim.data_ptr(), out.data_ptr(), n,
                                                     int(penalty), batch, st), "lego_nw_run")
     LAUNCHES[0] += 2
     return out
-
-
-def _check_out(out, shape, dtype, device, what):
-    """Caller-provided outputs go to the C ABI as bare pointers: check them."""
-    if out.dtype != dtype:
-        raise ShapeMismatch(f"{what}: out has dtype {out.dtype}, expected {dtype}")
-    if out.device != device:
-        raise ShapeMismatch(f"{what}: out is on {out.device}, expected {device}")
-    if not out.is_contiguous():
-        raise ShapeMismatch(f"{what}: out must be contiguous")
-    if tuple(out.shape) != tuple(shape):
-        raise ShapeMismatch(f"{what}: out has shape {tuple(out.shape)}, expected {tuple(shape)}")
 
 
 # measured (scripts/ab_gemm_group.py, 8192^3, 4 alternating runs each): G = 32 685 us,
@@ -671,8 +875,12 @@ def gemm(a, b, *, out=None, raster: Optional[int] = None, a_col: bool = False, b
     if raster is None:
         raster = GEMM_RASTER_GROUP
     torch = _torch()
-    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or not a.is_cuda:
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or not a.is_cuda or not b.is_cuda:
         raise ShapeMismatch("gemm takes CUDA bfloat16 tensors")
+    if a.device != b.device:
+        raise ShapeMismatch(f"gemm operands on different devices: {a.device} and {b.device}")
+    if a.dim() < 2 or b.dim() < 2 or tuple(a.shape[:-2]) != tuple(b.shape[:-2]):
+        raise ShapeMismatch(f"gemm needs matching batch dims: {tuple(a.shape)} vs {tuple(b.shape)}")
     a, b = a.contiguous(), b.contiguous()
     K, M = (a.shape[-2], a.shape[-1]) if a_col else (a.shape[-1], a.shape[-2])
     Kb, N = (b.shape[-2], b.shape[-1]) if b_col else (b.shape[-1], b.shape[-2])
@@ -683,14 +891,32 @@ def gemm(a, b, *, out=None, raster: Optional[int] = None, a_col: bool = False, b
         batch *= d
     if out is None:
         out = torch.empty(*a.shape[:-2], M, N, dtype=torch.bfloat16, device=a.device)
+    else:
+        _check_out(out, (*a.shape[:-2], M, N), torch.bfloat16, a.device, "gemm")
     if batch == 0 or M == 0 or N == 0:
         return out
     if K == 0:
         return out.zero_()
-    runtime.check(runtime.lib().lego_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K,
-                                                  batch, raster, int(a_col), int(b_col),
-                                                  runtime.stream_handle(stream)),
-                  "lego_gemm_bf16_ex")
+    with torch.cuda.device(a.device):
+        runtime.check(runtime.lib().lego_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K,
+                                                      batch, raster, int(a_col), int(b_col),
+                                                      runtime.stream_handle(stream)),
+                      "lego_gemm_bf16_ex")
+    LAUNCHES[0] += 1
+    return out
+
+
+def gemm_raster(mtiles: int, ntiles: int, batch: int = 1, group: Optional[int] = None, *, device=None):
+    """The GEMM kernels' tile order as the device evaluates it: row t of the
+    (mtiles*ntiles*batch, 3) int32 result is (batch, m-block, n-block) of
+    tile t.  ``group`` = G of the grouped raster (0 = row-major)."""
+    torch = _torch()
+    group = GEMM_RASTER_GROUP if group is None else group
+    dev = _device(device)
+    out = torch.empty(mtiles * ntiles * batch, 3, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        runtime.check(runtime.lib().lego_gemm_raster(out.data_ptr(), mtiles, ntiles, batch, group,
+                                                     runtime.stream_handle(None)), "lego_gemm_raster")
     LAUNCHES[0] += 1
     return out
 
@@ -706,7 +932,3 @@ def matmul(a, b, *, a_layout: str = "row", b_layout: str = "row", out=None, **kw
         raise ShapeMismatch("a_layout / b_layout must be 'row' or 'col'")
     # gemm computes A @ B'^T with B' = B^T given K-major (N x K) or MN-major (K x N)
     return gemm(a, b, out=out, a_col=a_layout == "col", b_col=b_layout == "row", **kw)
-
-
-def _ensure_var(v) -> Var:
-    return v

@@ -41,7 +41,6 @@ checked bit-exact against the same CPU DP (``tests/test_nw_layouts.py``).
 
 from __future__ import annotations
 
-import threading
 from typing import Optional, Tuple
 
 from . import codegen, lower, runtime
@@ -325,43 +324,24 @@ def program_source(parts: NwParts) -> Tuple[str, runtime.ProgramInfo, dict]:
     return src, info, defines
 
 
-class NwProgram:
-    """A compiled, proven wavefront program for one layout and n."""
-
-    def __init__(self, parts: NwParts, prog: runtime.Program, defines: dict):
-        self.parts, self.prog, self.defines = parts, prog, defines
-
-    def __repr__(self):
-        return f"NwProgram({self.parts!r}, {self.defines})"
-
-
-_NW_LOCK = threading.Lock()
-_NW_PROGRAMS = {}
-
-
-def nw_program(layout, n: int, device=None) -> NwProgram:
-    """Prove and compile (cached per layout, n and device)."""
+def nw_program(layout, n: int, device=None):
+    """Prove and compile (cached per layout, n and device by kernels'
+    program cache; equal generated sources share one loaded module).  The
+    returned program carries ``parts`` and ``defines``."""
     import torch
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    key = (layout, n, dev.index)
-    got = _NW_PROGRAMS.get(key)
-    if got is not None:
-        return got
-    with _NW_LOCK:
-        got = _NW_PROGRAMS.get(key)
-        if got is not None:
-            return got
+
+    from . import kernels as K
+    dev = K._device(device)
+
+    def build():
         parts = nw_parts(layout, n)
         check_tile_order(parts, device=dev)
         check_cell_order(parts, device=dev)
         src, info, defines = program_source(parts)
-        with torch.cuda.device(dev):
-            prog = runtime.Program(runtime.compile_cubin(src), info, src)
-        got = NwProgram(parts, prog, defines)
-        if len(_NW_PROGRAMS) >= 64:            # bounded: drop the oldest entry
-            _NW_PROGRAMS.pop(next(iter(_NW_PROGRAMS)))
-        _NW_PROGRAMS[key] = got
-    return got
+        return src, info, {"parts": parts, "defines": defines}
+
+    with torch.cuda.device(dev):
+        return K._program(("nw", K._layout_key(layout), n), build, dev.index)
 
 
 def describe(layout) -> str:

@@ -49,7 +49,7 @@ class ProgramInfo(ctypes.Structure):
                 ("reserved", ctypes.c_int32)]
 
 
-KIND_INDEX_MAP, KIND_GATHER, KIND_TRANSPOSE, KIND_BAND, KIND_SCATTER, KIND_STAGED, KIND_NW = 0, 1, 2, 3, 4, 5, 6
+KIND_INDEX_MAP, KIND_GATHER, KIND_TRANSPOSE, KIND_BAND, KIND_SCATTER, KIND_STAGED, KIND_NW, KIND_SOFTMAX = 0, 1, 2, 3, 4, 5, 6, 7
 # lego_program_info.reserved flags (include/lego_b200.h): element-aligned buffers suffice
 ALIGN_SRC_FREE, ALIGN_DST_FREE = 1, 2
 
@@ -73,10 +73,14 @@ SIGS = {
     "lego_apply_map": ([VP, VP, I32, I64, I64, VP], I32),
     "lego_inv_map": ([VP, VP, I32, I64, I64, VP], I32),
     "lego_check_bijective": ([VP, VP, ctypes.POINTER(I64), VP], I32),
+    "lego_check_injective": ([VP, VP, ctypes.POINTER(I64), VP], I32),
     "lego_remap": ([VP, VP, VP, I64, I64, I64, VP], I32),
     "lego_softmax_f32": ([VP, VP, I64, I64, VP], I32),
     "lego_nw_i32": ([VP, VP, I64, I32, I64, VP], I32),
     "lego_nw_run": ([VP, VP, VP, I64, I32, I64, VP], I32),
+    "lego_softmax_run": ([VP, VP, VP, I64, I64, VP], I32),
+    "lego_softmax_offsets": ([VP, VP, I64, VP], I32),
+    "lego_gemm_raster": ([VP, I64, I64, I64, I32, VP], I32),
     "lego_gemm_bf16": ([VP, VP, VP, I64, I64, I64, I64, I32, VP], I32),
     "lego_gemm_bf16_ex": ([VP, VP, VP, I64, I64, I64, I64, I32, I32, I32, VP], I32),
 }
