@@ -103,6 +103,19 @@ lego_status lego_program_load(const void *cubin, size_t cubin_len, const lego_pr
                               lego_program *out);
 void lego_program_release(lego_program p);
 
+/* --- user modules ---------------------------------------------------------
+ * Kernels a user writes as LEGO templates (template.instantiate with
+ * [target] cuda, reference template.py:444-537 + the new cuda profile of
+ * emit.py), compiled by lego_nvrtc_compile, loaded into the current
+ * device's primary context and launched by name; args as for
+ * cuLaunchKernel (an array of pointers to the argument values). */
+typedef struct lego_module_s *lego_module;
+lego_status lego_module_load(const void *cubin, size_t cubin_len, lego_module *out);
+void lego_module_release(lego_module m);
+lego_status lego_module_launch(lego_module m, const char *kernel, uint32_t gx, uint32_t gy, uint32_t gz,
+                               uint32_t bx, uint32_t by, uint32_t bz, uint32_t smem, void **args,
+                               void *stream);
+
 /* --- bulk layout evaluation ---------------------------------------------- */
 /* out[k] = apply(canon_unflatten(dims, first + k))  for k < count
  *   (a loop of GroupBy.apply, layout.py:313; ExpandBy masks give -1)

@@ -352,6 +352,46 @@ extern "C" lego_status lego_check_injective(lego_program p, uint32_t* hist, int6
     return check_hits(p, hist, violations, 1, stream);
 }
 
+// ---------------------------------------------------------------------------
+// user modules: kernels instantiated from LEGO templates (template.instantiate
+// with [target] cuda), compiled by lego_nvrtc_compile and launched by name
+// ---------------------------------------------------------------------------
+struct lego_module_s {
+    CUmodule_t mod = nullptr;
+};
+
+extern "C" lego_status lego_module_load(const void* cubin, size_t cubin_len, lego_module* out) {
+    (void)cubin_len;
+    if (!cubin || !out) return lego_fail(LEGO_E_ARG, "null argument");
+    lego_status s = load_driver();
+    if (s) return s;
+    if ((s = lego_cuda_check(cudaFree(nullptr), "cudaFree(0)"))) return s;
+    auto* m = new lego_module_s();
+    if ((s = drv_check(g_drv.load(&m->mod, cubin), "cuModuleLoadData"))) {
+        delete m;
+        return s;
+    }
+    *out = m;
+    return LEGO_OK;
+}
+
+extern "C" void lego_module_release(lego_module m) {
+    if (!m) return;
+    if (m->mod && g_drv.unload) g_drv.unload(m->mod);
+    delete m;
+}
+
+extern "C" lego_status lego_module_launch(lego_module m, const char* kernel, uint32_t gx, uint32_t gy, uint32_t gz,
+                                          uint32_t bx, uint32_t by, uint32_t bz, uint32_t smem, void** args,
+                                          void* stream) {
+    if (!m || !kernel) return lego_fail(LEGO_E_ARG, "null argument");
+    CUfunction_t fn = nullptr;
+    lego_status s = drv_check(g_drv.get_fn(&fn, m->mod, kernel), "cuModuleGetFunction");
+    if (s) return s;
+    if (smem > 48 * 1024 && (s = drv_check(g_drv.set_attr(fn, 8, (int)smem), "cuFuncSetAttribute"))) return s;
+    return drv_check(g_drv.launch(fn, gx, gy, gz, bx, by, bz, smem, stream, args, nullptr), "cuLaunchKernel");
+}
+
 extern "C" lego_status lego_softmax_run(lego_program p, const float* x, float* y, int64_t rows, int64_t cols,
                                         void* stream) {
     if (!p || p->info.kind != LEGO_PROG_SOFTMAX) return lego_fail(LEGO_E_ARG, "program is not a softmax program");

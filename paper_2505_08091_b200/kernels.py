@@ -89,7 +89,11 @@ class _ProgramCache:
                 return prog
         source, info, extra = builder()
         import hashlib
-        sk = (hashlib.sha256(source.encode()).hexdigest(), device)
+        # a loaded program is shared only between builds with the same text,
+        # geometry and plan facts (e.g. NW programs of equal text for two n)
+        facts = tuple(getattr(info, f) for f, _t in info._fields_)
+        plain = tuple(sorted((k, v) for k, v in (extra or {}).items() if isinstance(v, (int, str, bool))))
+        sk = (hashlib.sha256(source.encode()).hexdigest(), facts, plain, device)
         with self.lock:
             prog = self.by_source.get(sk)
         if prog is None:
@@ -134,8 +138,10 @@ def index_map_source(layout) -> Tuple[str, runtime.ProgramInfo]:
         f, inv = lower.inv_map_expr(layout)
         body += codegen.generate("inv_fn", [f], {"out": inv},
                                  bounds={"out": (0, lower.logical_size(layout) - 1)}).source
+    # positions of an injective-mode layout may run past its logical size
+    units = lower.value_range(app)[1] + 1 if injective else lower.physical_size(layout)
     info = runtime.ProgramInfo(kind=runtime.KIND_INDEX_MAP, elem_bytes=0,
-                               n=lower.logical_size(layout), units=lower.physical_size(layout),
+                               n=lower.logical_size(layout), units=max(units, 1),
                                unit_threads=1, block=256, smem_bytes=0)
     return _assemble(body, {"LEGO_KIND": 0}), info
 
@@ -634,7 +640,7 @@ def _check_hits(layout, fn_name, device, stream):
     torch = _torch()
     dev = _device(device)
     prog = _map_program(layout, dev.index)
-    hist = torch.empty(lower.physical_size(layout), dtype=torch.int32, device=dev)
+    hist = torch.empty(prog.info.units, dtype=torch.int32, device=dev)
     bad = runtime.I64()
     with torch.cuda.device(dev):
         runtime.check(getattr(runtime.lib(), fn_name)(prog.handle, hist.data_ptr(), ctypes.byref(bad),
@@ -904,6 +910,19 @@ def gemm(a, b, *, out=None, raster: Optional[int] = None, a_col: bool = False, b
                       "lego_gemm_bf16_ex")
     LAUNCHES[0] += 1
     return out
+
+
+def compile_template(template_text: str, manifest_text: str, layouts=None) -> "runtime.Module":
+    """Instantiate a LEGO ``.cu`` template (reference ``template.instantiate``,
+    template.py:522-537) with the ``cuda`` target profile, compile it for
+    sm_100a (NVRTC, cubin cached on disk) and load it: the paper's CUDA
+    integration route.  The manifest must select
+    ``[target] cuda``; the index helpers (floor div/mod, exact isqrt) are
+    prepended."""
+    from . import template as T
+    manifest = T.parse_manifest(manifest_text)
+    src = T.instantiate(T.parse_template(template_text), manifest, layouts=layouts)
+    return runtime.Module(runtime.compile_cubin(_text("lego_index.cuh") + "\n" + src))
 
 
 def gemm_raster(mtiles: int, ntiles: int, batch: int = 1, group: Optional[int] = None, *, device=None):

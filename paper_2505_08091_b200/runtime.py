@@ -70,6 +70,11 @@ SIGS = {
     "lego_free": ([VP], None),
     "lego_program_load": ([VP, ctypes.c_size_t, ctypes.POINTER(ProgramInfo), ctypes.POINTER(VP)], I32),
     "lego_program_release": ([VP], None),
+    "lego_module_load": ([VP, ctypes.c_size_t, ctypes.POINTER(VP)], I32),
+    "lego_module_release": ([VP], None),
+    "lego_module_launch": ([VP, ctypes.c_char_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                            ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                            ctypes.POINTER(VP), VP], I32),
     "lego_apply_map": ([VP, VP, I32, I64, I64, VP], I32),
     "lego_inv_map": ([VP, VP, I32, I64, I64, VP], I32),
     "lego_check_bijective": ([VP, VP, ctypes.POINTER(I64), VP], I32),
@@ -173,6 +178,34 @@ class Program:
         if h and _lib is not None:
             try:
                 _lib.lego_program_release(h)
+            except Exception:  # noqa: BLE001 - interpreter teardown
+                pass
+            self.handle = None
+
+
+class Module:
+    """A user kernel module (e.g. an instantiated LEGO ``.cu`` template)
+    compiled for sm_100a; ``launch`` runs one of its ``extern "C"`` kernels."""
+
+    def __init__(self, cubin: bytes):
+        self._cubin = ctypes.create_string_buffer(cubin, len(cubin))
+        h = VP()
+        check(lib().lego_module_load(self._cubin, len(cubin), ctypes.byref(h)), "lego_module_load")
+        self.handle = h
+
+    def launch(self, kernel: str, grid, block, args, *, smem: int = 0, stream=None):
+        """``args``: ctypes values (c_void_p for device pointers, c_int64, ...)."""
+        grid = tuple(grid) + (1,) * (3 - len(tuple(grid)))
+        block = tuple(block) + (1,) * (3 - len(tuple(block)))
+        ptrs = (VP * max(1, len(args)))(*[ctypes.cast(ctypes.pointer(a), VP) for a in args])
+        check(lib().lego_module_launch(self.handle, kernel.encode(), *grid, *block, smem, ptrs,
+                                       stream_handle(stream)), f"lego_module_launch({kernel})")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and _lib is not None:
+            try:
+                _lib.lego_module_release(h)
             except Exception:  # noqa: BLE001 - interpreter teardown
                 pass
             self.handle = None
