@@ -643,10 +643,13 @@ def other_kernels(args, pk, world):
         x = torch.arange(n_elems, device="cuda", dtype=torch.int64).to(dtype)
         src_l, dst_l = (None, layout) if direction == "to" else (layout, None)
         out = K.remap(x, src_l, dst_l)
-        fn = lambda: K.remap(x, src_l, dst_l, out=out)  # noqa: E731
-        plan = K.remap_plan(src_l, dst_l, x.element_size())
-        # bytes: each source element read once, each written destination element once
-        nbytes = (2 * x.numel() if scatter else x.numel() + out.numel()) * x.element_size()
+        # scatters into injective layouts run in fill mode: every destination
+        # position written once (hits from the source, the rest the fill value)
+        fill = 0 if scatter else None
+        fn = lambda: K.remap(x, src_l, dst_l, out=out, fill=fill)  # noqa: E731
+        plan = K.plan_remap(src_l, dst_l, x.element_size(), fill=scatter)
+        # bytes: each source element read once, each destination element written once
+        nbytes = (x.numel() + out.numel()) * x.element_size()
         hbm_entry(name, nbytes, fn, traffic_key, {"plan": repr(plan)})
         del x, out
     f1 = L.parse_layout("GroupBy([8192,8192]).OrderBy(RegP([128,64,128,64],[1,3,2,4]))"
@@ -669,10 +672,15 @@ def other_kernels(args, pk, world):
                       ("cfg4b_nw_tiles128_antidiag_i32", NW.nw_layout(16384, tile_rows=128, tile_order="antidiag"))]
         for name, lay in nw_layouts:
             K.nw_score(sim, 10, layout=lay, out=score)
+            prog = NW.nw_program(lay, 16384)
             ms = time_steps(lambda: K.nw_score(sim, 10, layout=lay, out=score), 5, 3, world) / 5
             res[name] = {"GCUPS": round(cells / (ms * 1e-3) / 1e9, 1), "us": round(ms * 1e3, 1),
                          "GB/s": round((cells * 4 + 16385 ** 2 * 4) / (ms * 1e-3) / 1e9, 1),
-                         "layout": NW.describe(lay), "path": "lego_nw_run (NVRTC program of the layout)"}
+                         "layout": NW.describe(lay),
+                         "path": ("lego_nw_run (NVRTC program of the layout: " + str(prog.defines) + ")"
+                                  if any(prog.defines.values()) else
+                                  "lego_nw_i32 (the layout lowers to no generated map: the library's "
+                                  "built-in instance of the template)")}
         del sim, score
     except Exception as exc:  # noqa: BLE001
         res["cfg4b_nw_wavefront_i32"] = {"unavailable": str(exc)[:200]}

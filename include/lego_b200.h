@@ -83,6 +83,11 @@ typedef struct {
 
 #define LEGO_ALIGN_SRC_FREE 1
 #define LEGO_ALIGN_DST_FREE 2
+/* scatter programs built with a fill mode (lego_remap_fill): FUSED = one
+ * kernel writes every destination position (affine injective layouts,
+ * whole 16-byte sectors); PASS = a vector fill, then the scatter */
+#define LEGO_FILL_FUSED 4
+#define LEGO_FILL_PASS 8
 
 int32_t lego_abi_version(void);
 const char *lego_last_error(void);
@@ -150,6 +155,12 @@ lego_status lego_check_injective(lego_program p, uint32_t *hist, int64_t *violat
  * peer route.peer(f), element offset route.off(f); batch must be 1. */
 lego_status lego_remap(lego_program p, const void *src, void *dst, int64_t batch,
                        int64_t src_stride, int64_t dst_stride, void *stream);
+/* Scatter into an injective-mode layout writing EVERY destination position:
+ * dst[apply(x)] = src[x], all other positions = *fill (elem_bytes bytes).
+ * Replaces "zero the destination, then scatter" (whose partial-sector
+ * stores force DRAM read-for-merge) for programs built with a fill mode. */
+lego_status lego_remap_fill(lego_program p, const void *src, void *dst, int64_t batch,
+                            int64_t src_stride, int64_t dst_stride, const void *fill, void *stream);
 
 /* --- fixed kernels with LEGO-derived layouts ------------------------------ */
 /* Row softmax, fp32, rows x cols row-major.  Rows in registers with float4

@@ -74,11 +74,18 @@ def _pool_chunk(args):
                       dtype=np.int64)
 
 
+def _threaded() -> bool:
+    """fork() is unsafe once CUDA (and its threads) is up in this process."""
+    import sys
+    torch = sys.modules.get("torch")
+    return bool(torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized())
+
+
 def _scalar_map(fn, inputs: np.ndarray, fwd: bool) -> np.ndarray:
     """fn applied element by element (fork pool for large inputs)."""
     global _POOL_FN
     n = len(inputs)
-    if n <= 1 << 14 or not hasattr(os, "fork"):
+    if n <= 1 << 14 or not hasattr(os, "fork") or _threaded():
         _POOL_FN = fn
         return _pool_chunk((inputs, fwd))
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()

@@ -191,7 +191,7 @@ extern "C" lego_status lego_nvrtc_compile(const char* source, size_t source_len,
 struct lego_program_s {
     lego_program_info info;
     CUmodule_t mod = nullptr;
-    CUfunction_t remap = nullptr;
+    CUfunction_t remap = nullptr, remap_fill = nullptr;
     CUfunction_t apply32 = nullptr, apply64 = nullptr, inv32 = nullptr, inv64 = nullptr;
     CUfunction_t hist = nullptr, hist_check = nullptr;
     CUfunction_t nw_tiles = nullptr, nw_borders = nullptr;
@@ -262,6 +262,13 @@ extern "C" lego_status lego_program_load(const void* cubin, size_t cubin_len,
         }
         if (info->smem_bytes > 48 * 1024)
             g_drv.set_attr(p->remap, 8 /*CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES*/, info->smem_bytes);
+        if ((info->reserved & (LEGO_FILL_FUSED | LEGO_FILL_PASS)) &&
+            (s = drv_check(g_drv.get_fn(&p->remap_fill, p->mod, "lego_remap_fill"),
+                           "cuModuleGetFunction(lego_remap_fill)"))) {
+            g_drv.unload(p->mod);
+            delete p;
+            return s;
+        }
     }
     *out = p;
     return LEGO_OK;
@@ -437,8 +444,41 @@ extern "C" lego_status lego_nw_run(lego_program p, const int32_t* sim, int32_t* 
     return launch(p->nw_tiles, pl.ctas, 1, 128, (unsigned)pl.smem, stream, a2);
 }
 
+static lego_status remap_args(lego_program p, const void* src, void* dst, int64_t batch, int64_t src_stride,
+                              int64_t dst_stride);
+
+extern "C" lego_status lego_remap_fill(lego_program p, const void* src, void* dst, int64_t batch,
+                                       int64_t src_stride, int64_t dst_stride, const void* fill, void* stream) {
+    if (!p || !(p->info.reserved & (LEGO_FILL_FUSED | LEGO_FILL_PASS)))
+        return lego_fail(LEGO_E_ARG, "program was not built with a fill mode");
+    if (!fill) return lego_fail(LEGO_E_ARG, "null fill value");
+    lego_status s = remap_args(p, src, dst, batch, src_stride, dst_stride);
+    if (s || batch == 0) return s;
+    unsigned long long bits = 0;
+    memcpy(&bits, fill, (size_t)p->info.elem_bytes);
+    void* args[] = {&src, &dst, &src_stride, &dst_stride, &bits};
+    if (p->info.reserved & LEGO_FILL_FUSED)
+        return launch(p->remap_fill, (unsigned)p->info.units, (unsigned)batch, (unsigned)p->info.block, 0, stream,
+                      args);
+    if ((s = launch(p->remap_fill, 148 * 4, (unsigned)batch, 256, 0, stream, args))) return s;
+    void* a2[] = {&src, &dst, &src_stride, &dst_stride};
+    return launch(p->remap, (unsigned)p->info.units, (unsigned)batch, (unsigned)p->info.block,
+                  (unsigned)p->info.smem_bytes, stream, a2);
+}
+
 extern "C" lego_status lego_remap(lego_program p, const void* src, void* dst, int64_t batch,
                                   int64_t src_stride, int64_t dst_stride, void* stream) {
+    lego_status s = remap_args(p, src, dst, batch, src_stride, dst_stride);
+    if (s || batch == 0) return s;
+    if (p->info.reserved & LEGO_FILL_FUSED)
+        return lego_fail(LEGO_E_ARG, "fused fill program: call lego_remap_fill");
+    void* args[] = {&src, &dst, &src_stride, &dst_stride};
+    return launch(p->remap, (unsigned)p->info.units, (unsigned)batch, (unsigned)p->info.block,
+                  (unsigned)p->info.smem_bytes, stream, args);
+}
+
+static lego_status remap_args(lego_program p, const void* src, void* dst, int64_t batch, int64_t src_stride,
+                              int64_t dst_stride) {
     if (!p || p->info.kind == LEGO_PROG_INDEX_MAP)
         return lego_fail(LEGO_E_ARG, "program is not a remap program");
     if (batch < 0) return lego_fail(LEGO_E_ARG, "negative batch");
@@ -455,7 +495,5 @@ extern "C" lego_status lego_remap(lego_program p, const void* src, void* dst, in
         return lego_fail(LEGO_E_ARG, "buffers must be 16-byte aligned");
     if (batch > 1 && ((src_vec && ((src_stride * e) & 15)) || (dst_vec && ((dst_stride * e) & 15))))
         return lego_fail(LEGO_E_ARG, "batch strides must be multiples of 16 bytes");
-    void* args[] = {&src, &dst, &src_stride, &dst_stride};
-    return launch(p->remap, (unsigned)p->info.units, (unsigned)batch, (unsigned)p->info.block,
-                  (unsigned)p->info.smem_bytes, stream, args);
+    return LEGO_OK;
 }

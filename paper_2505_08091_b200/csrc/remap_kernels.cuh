@@ -139,12 +139,73 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_apply_map_i32(int* out, long long f
 LEGO_GLOBAL void __launch_bounds__(256) lego_apply_map_i64(long long* out, long long first, long long count) {
     lego_map_body<long long, 4>(out, first, count, 0);
 }
+#if LEGO_INV_RUNS
+// Inverse of an n x n layout whose positions run contiguously along
+// anti-diagonals (kernels.index_map_source proved
+// apply(i+1, j-1) == apply(i, j) + 1 symbolically, lower.diagonal_runs_contiguous):
+// position f+1 holds (i+1, j-1) while that cell exists, so a thread
+// evaluates the generated inverse (isqrt and selects) once for its first
+// position and steps along the run for the rest -- logical row-major index
+// + (n - 1) per position -- re-evaluating only where a diagonal ends.
+template <typename T, int G>
+static __device__ __forceinline__ void lego_inv_runs_body(T* out, long long first, long long count) {
+    constexpr long long NN = gen::RUN_N;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long done = 0;
+    if ((reinterpret_cast<unsigned long long>(out) & 15) == 0) {
+        const long long nq = count / G;
+        for (long long q = tid; q < nq; q += stride) {
+            const long long x = first + G * q;
+            T v[G];
+            long long r;
+            gen::inv_fn(x, r);
+            long long i = r / NN, j = r - i * NN;
+            v[0] = (T)r;
+#pragma unroll
+            for (int u = 1; u < G; ++u) {
+                if (j > 0 && i + 1 < NN) {
+                    ++i;
+                    --j;
+                    r += NN - 1;
+                } else {
+                    gen::inv_fn(x + u, r);
+                    i = r / NN;
+                    j = r - i * NN;
+                }
+                v[u] = (T)r;
+            }
+#pragma unroll
+            for (int g = 0; g < G / 4; ++g) {
+                T* o = out + G * q + 4 * g;
+                if (sizeof(T) == 4) {
+                    *reinterpret_cast<int4*>(o) = make_int4((int)v[4 * g], (int)v[4 * g + 1], (int)v[4 * g + 2],
+                                                            (int)v[4 * g + 3]);
+                } else {
+                    *reinterpret_cast<longlong2*>(o) = make_longlong2((long long)v[4 * g], (long long)v[4 * g + 1]);
+                    *reinterpret_cast<longlong2*>(o + 2) = make_longlong2((long long)v[4 * g + 2],
+                                                                          (long long)v[4 * g + 3]);
+                }
+            }
+        }
+        done = nq * G;
+    }
+    for (long long k = done + tid; k < count; k += stride) out[k] = lego_map_one<T>(first + k, 1);
+}
+LEGO_GLOBAL void __launch_bounds__(256) lego_inv_map_i32(int* out, long long first, long long count) {
+    lego_inv_runs_body<int, LEGO_INV_RUNS>(out, first, count);
+}
+LEGO_GLOBAL void __launch_bounds__(256) lego_inv_map_i64(long long* out, long long first, long long count) {
+    lego_inv_runs_body<long long, LEGO_INV_RUNS>(out, first, count);
+}
+#else
 LEGO_GLOBAL void __launch_bounds__(256) lego_inv_map_i32(int* out, long long first, long long count) {
     lego_map_body<int, 8>(out, first, count, 1);
 }
 LEGO_GLOBAL void __launch_bounds__(256) lego_inv_map_i64(long long* out, long long first, long long count) {
     lego_map_body<long long, 8>(out, first, count, 1);
 }
+#endif
 // histogram of apply over the whole logical space (bijectivity proof)
 LEGO_GLOBAL void __launch_bounds__(256) lego_hist(unsigned int* hist, long long count, long long n_out,
                                                   unsigned long long* bad) {
@@ -619,6 +680,78 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
     }
 }
 #endif  // LEGO_SCALAR
+
+#if LEGO_FILL
+// Fill mode: every destination position is written -- hit positions with
+// their source element, the others with `fill` (raw element bits) -- so the
+// destination needs no prior initialisation and no read-for-merge.
+#if LEGO_FK > 0
+// The planner proved apply(x) = FK*x + FC over the whole source (an affine
+// injective layout, e.g. the even map FK = 2): source vector q (V elements)
+// owns the destination window [FK*V*q + FC, FK*V*(q+1) + FC) of FK whole
+// 16-byte vectors, which it assembles in registers and stores in full
+// sectors; windows tile the destination.  Threads of q < ceil(FC/V) also
+// fill the prefix [0, FC); the last window is clipped at N_DST.
+LEGO_GLOBAL void __launch_bounds__(256) lego_remap_fill(const unsigned char* __restrict__ src,
+                                                        unsigned char* __restrict__ dst,
+                                                        long long src_stride, long long dst_stride,
+                                                        unsigned long long fill) {
+    const unsigned char* s = src + (long long)blockIdx.y * src_stride * LEGO_ELEM;
+    lego_e* d = reinterpret_cast<lego_e*>(dst + (long long)blockIdx.y * dst_stride * LEGO_ELEM);
+    const lego_e fv = (lego_e)fill;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q * LEGO_VEC < LEGO_FC) {
+#pragma unroll
+        for (int k = 0; k < LEGO_VEC; ++k)
+            if (q * LEGO_VEC + k < LEGO_FC) d[q * LEGO_VEC + k] = fv;
+    }
+    if (q >= gen::N / LEGO_VEC) return;
+    union { lego_v16 v; lego_e e[LEGO_VEC]; } in;
+    in.v = lego_ld16(s + q * 16);
+    const long long w0 = (long long)LEGO_FK * LEGO_VEC * q + LEGO_FC;
+#pragma unroll
+    for (int j = 0; j < LEGO_FK; ++j) {
+        union { lego_v16 v; lego_e e[LEGO_VEC]; } out;
+#pragma unroll
+        for (int m = 0; m < LEGO_VEC; ++m) {
+            const int w = j * LEGO_VEC + m;
+            out.e[m] = (w % LEGO_FK == 0) ? in.e[w / LEGO_FK] : fv;
+        }
+        const long long p = w0 + (long long)j * LEGO_VEC;
+        if (p + LEGO_VEC <= gen::N_DST) {
+            lego_st16(reinterpret_cast<unsigned char*>(d + p), out.v);
+        } else {
+#pragma unroll
+            for (int m = 0; m < LEGO_VEC; ++m)
+                if (p + m < gen::N_DST) d[p + m] = out.e[m];
+        }
+    }
+}
+#else
+// General injective layouts: a vector fill of [0, N_DST) ahead of the scatter
+// (lego_remap above), stream-ordered by the runtime.
+LEGO_GLOBAL void __launch_bounds__(256) lego_remap_fill(const unsigned char* __restrict__ src,
+                                                        unsigned char* __restrict__ dst,
+                                                        long long src_stride, long long dst_stride,
+                                                        unsigned long long fill) {
+    (void)src;
+    (void)src_stride;
+    lego_e* d = reinterpret_cast<lego_e*>(dst + (long long)blockIdx.y * dst_stride * LEGO_ELEM);
+    const lego_e fv = (lego_e)fill;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long mis = (reinterpret_cast<unsigned long long>(d) & 15) / LEGO_ELEM;
+    const long long head = mis ? (long long)(LEGO_VEC - mis) < gen::N_DST ? LEGO_VEC - mis : gen::N_DST : 0;
+    for (long long k = t; k < head; k += stride) d[k] = fv;
+    union { lego_v16 v; lego_e e[LEGO_VEC]; } u;
+#pragma unroll
+    for (int m = 0; m < LEGO_VEC; ++m) u.e[m] = fv;
+    const long long nv = (gen::N_DST - head) / LEGO_VEC;
+    for (long long k = t; k < nv; k += stride) lego_st16(reinterpret_cast<unsigned char*>(d + head + k * LEGO_VEC), u.v);
+    for (long long k = head + nv * LEGO_VEC + t; k < gen::N_DST; k += stride) d[k] = fv;
+}
+#endif  // LEGO_FK
+#endif  // LEGO_FILL
 #endif
 
 // ---------------------------------------------------------------------------

@@ -128,6 +128,7 @@ def _program(key, builder, device: int):
 def index_map_source(layout) -> Tuple[str, runtime.ProgramInfo]:
     x, app = lower.apply_map_expr(layout)
     injective = getattr(lower._group(layout), "injective", False)
+    defines = {"LEGO_KIND": 0}
     body = codegen.constant("N", lower.logical_size(layout))
     body += codegen.constant("M", lower.physical_size(layout))
     body += codegen.generate("apply_fn", [x], {"out": app},
@@ -138,12 +139,20 @@ def index_map_source(layout) -> Tuple[str, runtime.ProgramInfo]:
         f, inv = lower.inv_map_expr(layout)
         body += codegen.generate("inv_fn", [f], {"out": inv},
                                  bounds={"out": (0, lower.logical_size(layout) - 1)}).source
+        side = lower.antidiag_side(layout)
+        if INV_RUNS and side is not None and side > 1 and lower.diagonal_runs_contiguous(layout, side):
+            body += codegen.constant("RUN_N", side)
+            defines["LEGO_INV_RUNS"] = INV_RUNS
     # positions of an injective-mode layout may run past its logical size
     units = lower.value_range(app)[1] + 1 if injective else lower.physical_size(layout)
     info = runtime.ProgramInfo(kind=runtime.KIND_INDEX_MAP, elem_bytes=0,
                                n=lower.logical_size(layout), units=max(units, 1),
                                unit_threads=1, block=256, smem_bytes=0)
-    return _assemble(body, {"LEGO_KIND": 0}), info
+    return _assemble(body, defines), info
+
+
+# positions per thread of the run-walking inverse map (0 disables it)
+INV_RUNS = int(os.environ.get("LEGO_INV_RUNS", "8"))
 
 
 class RemapPlan:
@@ -170,7 +179,11 @@ class Route:
         self.world, self.fn, self.key = world, fn, key
 
 
-def plan_remap(src_layout, dst_layout, elem_bytes: int, route: Optional[Route] = None) -> RemapPlan:
+def plan_remap(src_layout, dst_layout, elem_bytes: int, route: Optional[Route] = None,
+               fill: bool = False) -> RemapPlan:
+    """``fill``: scatters into injective layouts write every destination
+    position (unhit ones with a fill value); other kinds write every
+    position anyway and ignore it."""
     if elem_bytes not in (1, 2, 4, 8, 16):
         raise UnsupportedNode(f"element size {elem_bytes} not supported (1, 2, 4, 8 or 16 bytes)")
     if route is not None:
@@ -178,7 +191,7 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int, route: Optional[Route] =
     band = _band_plan(src_layout, dst_layout, elem_bytes)
     if band is not None:
         return band
-    scatter = _scatter_plan(src_layout, dst_layout, elem_bytes)
+    scatter = _scatter_plan(src_layout, dst_layout, elem_bytes, fill)
     if scatter is not None:
         return scatter
     f, g, n_dst, n_src = lower.gather_expr(src_layout, dst_layout)
@@ -447,9 +460,23 @@ def _band_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
                      f"{'scatter' if direction == 0 else 'gather'}")
 
 
-def _scatter_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
+def _affine(e, x: Var, n: int):
+    """(k, c) with e(x) == k*x + c for every x in [0, n), else None."""
+    if n < 2:
+        return None
+    c = lower.value_at(e, x, 0)
+    k = lower.value_at(e, x, 1) - c
+    if c is None or k < 1:
+        return None
+    return (k, c) if lower.simplify(e - (x * k + c)) == IntConst(0) else None
+
+
+def _scatter_plan(src_layout, dst_layout, elem_bytes, fill=False) -> Optional[RemapPlan]:
     """Row-major source into an injective-mode layout (no inverse exists):
-    a true scatter, dst[apply(x)] = src[x] (LEGO_KIND 4)."""
+    a true scatter, dst[apply(x)] = src[x] (LEGO_KIND 4).  With ``fill``
+    every destination position is written: affine maps apply(x) = k*x + c
+    (proven symbolically) get one kernel assembling whole 16-byte windows in
+    registers; others a vector fill pass ahead of the scatter."""
     if src_layout is not None or dst_layout is None:
         return None
     if not getattr(lower._group(dst_layout), "injective", False):
@@ -461,25 +488,39 @@ def _scatter_plan(src_layout, dst_layout, elem_bytes) -> Optional[RemapPlan]:
     vec = 16 // elem_bytes
     scalar = n_src % vec != 0                               # ragged: one element per thread
     n_dst = lower.value_range(app)[1] + 1                   # highest position + 1
-    body = codegen.constant("N", n_src) + codegen.generate("pos_of", [x], {"p": app}).source
+    body = codegen.constant("N", n_src) + codegen.constant("N_DST", n_dst)
+    body += codegen.generate("pos_of", [x], {"p": app}).source
     units = max(1, min((n_src + 255) // 256, 148 * 16)) if scalar else (n_src // vec + 255) // 256
+    reserved = runtime.ALIGN_DST_FREE | (runtime.ALIGN_SRC_FREE if scalar else 0)
+    defines = {"LEGO_KIND": 4, "LEGO_ELEM": elem_bytes, "LEGO_SCALAR": int(scalar), "LEGO_FILL": int(fill)}
+    detail = f"scatter into an injective layout, {n_dst} positions"
+    if fill:
+        aff = None if scalar else _affine(app, x, n_src)
+        if aff is not None and (aff[1] * elem_bytes) % 16 == 0:
+            k, c = aff
+            defines.update({"LEGO_FK": k, "LEGO_FC": c})
+            units = (max(n_src // vec, -(-c // vec)) + 255) // 256
+            reserved = runtime.FILL_FUSED                   # 16-byte windows on both sides
+            detail += f", fill: affine {k}x+{c}, whole-sector windows"
+        else:
+            defines.update({"LEGO_FK": 0, "LEGO_FC": 0})
+            reserved |= runtime.FILL_PASS
+            detail += ", fill: vector fill pass + scatter"
     info = runtime.ProgramInfo(kind=runtime.KIND_SCATTER, elem_bytes=elem_bytes, n=n_src,
-                               units=units, unit_threads=1, block=256, smem_bytes=0,
-                               reserved=runtime.ALIGN_DST_FREE | (runtime.ALIGN_SRC_FREE if scalar else 0))
-    src = _assemble(body, {"LEGO_KIND": 4, "LEGO_ELEM": elem_bytes, "LEGO_SCALAR": int(scalar)})
-    return RemapPlan(runtime.KIND_SCATTER, n_dst, n_src, elem_bytes, False, False, src, info,
-                     f"scatter into an injective layout, {n_dst} positions")
+                               units=units, unit_threads=1, block=256, smem_bytes=0, reserved=reserved)
+    src = _assemble(body, defines)
+    return RemapPlan(runtime.KIND_SCATTER, n_dst, n_src, elem_bytes, False, False, src, info, detail)
 
 
-def _remap_program(src_layout, dst_layout, elem_bytes, device: int, route=None):
-    key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes,
+def _remap_program(src_layout, dst_layout, elem_bytes, device: int, route=None, fill: bool = False):
+    key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, fill,
            None if route is None else ("route", route.world, route.key), TRANSPOSE_VARIANT,
            BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB,
            BAND_ROWS, BAND_DIAGS, BAND_WARPS, TRANSPOSE_WARPS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE,
            staging.BOX_BULK, staging.BOX_THREADS)
 
     def build():
-        plan = plan_remap(src_layout, dst_layout, elem_bytes, route)
+        plan = plan_remap(src_layout, dst_layout, elem_bytes, route, fill)
         # the sizes it was planned for travel with the program (set before publication)
         return plan.source, plan.info, {"n_dst": plan.n_dst, "n_src": plan.n_src, "kind": plan.kind,
                                         "gated": _needs_bijectivity_gate(src_layout, dst_layout, plan)}
@@ -671,17 +712,24 @@ def remap_plan(src_layout, dst_layout, elem_bytes: int) -> RemapPlan:
     return plan_remap(src_layout, dst_layout, elem_bytes)
 
 
-def remap(src, src_layout=None, dst_layout=None, *, out=None, stream=None):
+def remap(src, src_layout=None, dst_layout=None, *, out=None, fill=None, stream=None):
     """Move ``src`` (shape ``(..., n_src)``) into the destination layout:
     for every logical index x, ``out[..., dst.apply(x)] = src[..., src.apply(x)]``.
-    ``None`` on either side means row-major over the other side's dims."""
+    ``None`` on either side means row-major over the other side's dims.
+
+    Injective-mode destinations (no inverse) leave positions no x hits:
+    with ``out`` given and ``fill=None`` they keep ``out``'s values;
+    otherwise they are set to ``fill`` (default 0 for a fresh output) by the
+    same launch.  Other layouts write every position; ``fill`` is unused."""
     torch = _torch()
     if not src.is_cuda:
         raise ShapeMismatch("remap takes a CUDA tensor (no CPU path)")
     elem = src.element_size()
     lower.check_pair(src_layout, dst_layout)
     dev = src.device
-    prog = _remap_program(src_layout, dst_layout, elem, dev.index)
+    injective = dst_layout is not None and getattr(lower._group(dst_layout), "injective", False)
+    want_fill = injective and src_layout is None and (fill is not None or out is None)
+    prog = _remap_program(src_layout, dst_layout, elem, dev.index, fill=want_fill)
     f_dst, n_src = prog.n_dst, prog.n_src
     if src.numel() % n_src:
         raise ShapeMismatch(f"source of {src.numel()} elements is not a batch of layouts of "
@@ -690,22 +738,30 @@ def remap(src, src_layout=None, dst_layout=None, *, out=None, stream=None):
     batch = src.numel() // n_src
     batch_shape = tuple(src.shape[:-1]) if src.dim() and src.shape[-1] == n_src else (batch,)
     if out is None:
-        alloc = torch.zeros if prog.info.kind == runtime.KIND_SCATTER else torch.empty
-        out = alloc(*batch_shape, f_dst, dtype=src.dtype, device=dev)
+        out = torch.empty(*batch_shape, f_dst, dtype=src.dtype, device=dev)
     else:
         _check_out(out, None, src.dtype, dev, "remap", min_numel=batch * f_dst)
     if batch == 0:
         return out
     _run_gates(prog, dev)
+    fill_buf = None
+    if want_fill:
+        fill_buf = torch.tensor([fill if fill is not None else 0], dtype=src.dtype).view(torch.uint8).numpy()
+        fill_buf = ctypes.create_string_buffer(fill_buf.tobytes(), elem)
     with torch.cuda.device(dev):
         st = runtime.stream_handle(stream)
         done = 0
         while done < batch:
             b = min(65535, batch - done)
-            runtime.check(runtime.lib().lego_remap(
-                prog.handle, src.data_ptr() + done * n_src * elem, out.data_ptr() + done * f_dst * elem,
-                b, n_src, f_dst, st), "lego_remap")
-            LAUNCHES[0] += 1
+            s_ptr, d_ptr = src.data_ptr() + done * n_src * elem, out.data_ptr() + done * f_dst * elem
+            if fill_buf is not None:
+                runtime.check(runtime.lib().lego_remap_fill(prog.handle, s_ptr, d_ptr, b, n_src, f_dst, fill_buf, st),
+                              "lego_remap_fill")
+                LAUNCHES[0] += 1 if prog.info.reserved & runtime.FILL_FUSED else 2
+            else:
+                runtime.check(runtime.lib().lego_remap(prog.handle, s_ptr, d_ptr, b, n_src, f_dst, st),
+                              "lego_remap")
+                LAUNCHES[0] += 1
             done += b
     return out
 
@@ -858,8 +914,14 @@ def nw_score(sim, penalty: int, *, layout=None, out=None, stream=None):
         else:
             from . import nw
             prog = nw.nw_program(layout, n, device=sim.device)
-            runtime.check(runtime.lib().lego_nw_run(prog.handle, sim.data_ptr(), out.data_ptr(), n,
-                                                    int(penalty), batch, st), "lego_nw_run")
+            if not any(prog.defines.values()):
+                # the layout lowers to no generated map (row-major strips, row-major
+                # ring): the library's nvcc-built instance of the same template
+                runtime.check(runtime.lib().lego_nw_i32(sim.data_ptr(), out.data_ptr(), n, int(penalty), batch,
+                                                        st), "lego_nw_i32")
+            else:
+                runtime.check(runtime.lib().lego_nw_run(prog.handle, sim.data_ptr(), out.data_ptr(), n,
+                                                        int(penalty), batch, st), "lego_nw_run")
     LAUNCHES[0] += 2
     return out
 

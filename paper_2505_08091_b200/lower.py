@@ -326,3 +326,9 @@ def diagonal_runs_contiguous(layout, n: int) -> bool:
 
 def value_range(e: Expr):
     return Intervals().of(e)
+
+
+def value_at(e: Expr, x: Var, v: int) -> Optional[int]:
+    """e with x = v, if it folds to a constant."""
+    got = simplify(substitute(e, {x.name: IntConst(v)}))
+    return got.value if type(got) is IntConst else None

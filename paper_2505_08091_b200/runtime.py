@@ -52,6 +52,7 @@ class ProgramInfo(ctypes.Structure):
 KIND_INDEX_MAP, KIND_GATHER, KIND_TRANSPOSE, KIND_BAND, KIND_SCATTER, KIND_STAGED, KIND_NW, KIND_SOFTMAX = 0, 1, 2, 3, 4, 5, 6, 7
 # lego_program_info.reserved flags (include/lego_b200.h): element-aligned buffers suffice
 ALIGN_SRC_FREE, ALIGN_DST_FREE = 1, 2
+FILL_FUSED, FILL_PASS = 4, 8
 
 _lib = None
 _lock = threading.Lock()
@@ -80,6 +81,7 @@ SIGS = {
     "lego_check_bijective": ([VP, VP, ctypes.POINTER(I64), VP], I32),
     "lego_check_injective": ([VP, VP, ctypes.POINTER(I64), VP], I32),
     "lego_remap": ([VP, VP, VP, I64, I64, I64, VP], I32),
+    "lego_remap_fill": ([VP, VP, VP, I64, I64, I64, VP, VP], I32),
     "lego_softmax_f32": ([VP, VP, I64, I64, VP], I32),
     "lego_nw_i32": ([VP, VP, I64, I32, I64, VP], I32),
     "lego_nw_run": ([VP, VP, VP, I64, I32, I64, VP], I32),

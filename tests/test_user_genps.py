@@ -100,19 +100,23 @@ def test_device_maps_and_remaps(name):
     lay = FACTORIES[name](L)
     app = C.apply_all(lay)
     assert np.array_equal(K.apply_map(lay, dtype=torch.int64).cpu().numpy(), app)
+    inv = None if lay.injective else C.inv_all(lay)
     if lay.injective:
         with pytest.raises(L.LegoError):
             K.inv_map(lay)
     else:
-        assert np.array_equal(K.inv_map(lay, dtype=torch.int64).cpu().numpy(), C.inv_all(lay))
+        assert np.array_equal(K.inv_map(lay, dtype=torch.int64).cpu().numpy(), inv)
     n = len(app)
     rng = np.random.default_rng(3)
     for dt in DTYPES:
         info = np.iinfo(dt)
         x = rng.integers(info.min, info.max, size=n, dtype=dt, endpoint=True)
         xd = torch.from_numpy(x).cuda()
-        got = K.remap(xd, None, lay).cpu().numpy()
-        assert np.array_equal(got, C.remap(x, None, lay, dst_size=got.size)), (name, dt, "scatter")
+        got = K.remap(xd, None, lay).cpu().numpy()                   # scatter: out[apply(x)] = x
+        want = np.zeros(got.size, dtype=dt)
+        want[app] = x
+        assert np.array_equal(got, want), (name, dt, "scatter")
         if not lay.injective:
-            got = K.remap(xd, lay, None).cpu().numpy()
-            assert np.array_equal(got, C.remap(x, lay, None)), (name, dt, "gather")
+            got = K.remap(xd, lay, None).cpu().numpy()               # gather: out[x] = src[apply(x)]
+            assert np.array_equal(got, x[app]), (name, dt, "gather")
+            assert np.array_equal(x[app][inv], x)
