@@ -75,7 +75,7 @@ def test_scatter_through_user_genp_is_gated():
     assert K.LAUNCHES[0] - prog_before == 3                     # histogram + check + scatter
     assert torch.equal(out[::2], x) and not out[1::2].any()
     prog_before = K.LAUNCHES[0]
-    K.remap(x, None, ok, out=out)                                # proven once per program
+    K.remap(x, None, ok, out=out, fill=0)                        # proven once per program
     assert K.LAUNCHES[0] - prog_before == 1
     bad = L.GroupBy([n], orders=(L.OrderBy(_even(n, collide=True)),), injective=True)
     with pytest.raises(L.BijectivityViolation):
