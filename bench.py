@@ -273,6 +273,24 @@ def cpu_remap_rate(target_seconds=10.0):
     return sample.run()
 
 
+def reference_python_rate():
+    """The reference package's own per-element Python path (BASELINE.md
+    4(i)), timed in the build container where the reference exists
+    (scripts/time_reference_python.py -> profiles/r02_reference_python.json);
+    reported beside the C port, not re-measured here."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_reference_python.json")) as fh:
+            d = json.load(fh)
+        c2 = d["layouts"]["cfg2"]
+        return {"elements_per_s": c2["elements_per_s"], "GB/s_equivalent": round(c2["elements_per_s"] * 4 / 1e9, 6),
+                "cores": d["cores"], "cpu": d.get("lscpu_model", d.get("cpu")),
+                "sample": f"{d['sample_points']} points of the headline layout, reference layout.apply per element "
+                          "on multiprocessing.Pool(all cores), measured in the build container "
+                          "(profiles/r02_reference_python.json)"}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -399,7 +417,9 @@ def run(args):
     t1.record(main)
     t1.synchronize()
     e2e_ms = max_over_ranks(t0.elapsed_time(t1), world) / e2e_steps
-    ok_e2e = torch.equal(host_out[(e2e_counter[0] - 1) & 1][:4096].cuda(), dev_out[(e2e_counter[0] - 1) & 1][:4096])
+    # the whole last result, as it arrived in host memory, against the
+    # device-timed path's output for the same input (bit-exact, all 2^28 elements)
+    ok_e2e = torch.equal(host_out[(e2e_counter[0] - 1) & 1].cuda(), out)
     e2e_value = world * 2 * nbytes / (e2e_ms * 1e-3) / 1e9
 
     kernels = {}
@@ -409,6 +429,9 @@ def run(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_remap_rate()
+        ref_py = reference_python_rate()
+        if ref_py:
+            cpu["reference_python"] = ref_py
 
     if rank == 0:
         line = {
