@@ -11,7 +11,7 @@ for k in ${KERNELS:-transpose band nw}; do
   case $k in
     gemm) pat="regex:gemm_bf16";;
     softmax) pat="regex:softmax_rows";;
-    nw) pat="regex:nw_strips";;
+    nw) pat="regex:lego_nw_tiles";;
     apply_map) pat="regex:lego_inv_map";;
     *) pat="regex:lego_remap";;
   esac

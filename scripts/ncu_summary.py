@@ -25,7 +25,7 @@ ALGO = {  # algorithmic bytes per launch of the captured workload (scripts/one_k
     "transpose": 2 * 16384 * 16384 * 2, "gather": 2 * 8 * 4096 * 4096 * 4,
     "band": 2 * 16384 * 16384 * 4, "softmax": 2 * 8192 * 8192 * 4,
     "nw": 16384 * 16384 * 4 + 16385 * 16385 * 4, "apply_map": 16384 * 16384 * 4,
-    "staged": 2 * 8192 * 8192 * 4, "scatter": 2 * (1 << 26) * 4, "expand": (8192 * 8192 + 8000 * 8000) * 4,
+    "staged": 2 * 8192 * 8192 * 4, "scatter": ((1 << 26) + (1 << 27) - 1) * 4, "expand": (8192 * 8192 + 8000 * 8000) * 4,
 }
 KEYS = {"transpose": "remap_transpose_bf16", "gather": "remap_gather_fp32", "band": "remap_antidiag_i32",
         "softmax": "softmax_fp32", "nw": "nw_wavefront_i32", "apply_map": "inv_map_antidiag_i32",

@@ -66,7 +66,7 @@ elif name == "scatter":
     g = L.GroupBy([1 << 26], orders=(L.OrderBy(even),), injective=True)
     x = torch.arange(1 << 26, device="cuda", dtype=torch.int32)
     y = K.remap(x, None, g)
-    fn = lambda: K.remap(x, None, g, out=y)  # noqa: E731
+    fn = lambda: K.remap(x, None, g, out=y, fill=0)  # noqa: E731   (fill mode: every position written)
 else:
     raise SystemExit(f"unknown kernel {name}")
 for _ in range(reps):
