@@ -205,10 +205,14 @@ __device__ __forceinline__ int slot(int r, int g, int h) {
 // compute-warp state: S' of the lane's 4 columns in its last finished row,
 // the diagonal predecessor of its first column, the last-column values it
 // sends right, and sim rows prefetched two steps ahead
+#ifndef NW_EARLY_SHFL
+#define NW_EARLY_SHFL 1          // shuffle each row's last column as soon as it is final (hides SHFL latency)
+#endif
 struct Lane {
     int h[CPL];
     int dprev;
     int send[RPS];
+    int lin[RPS];            // NW_EARLY_SHFL: the left neighbour's send[] of the previous step, already shuffled
     int4 nx1[RPS], nx2[RPS];
     int bv[RPS];
 };
@@ -293,7 +297,9 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, int4* ring4, u
     int left[RPS];
 #pragma unroll
     for (int q = 0; q < RPS; ++q) {
-#ifndef NW_ABL_NOSHFL
+#if NW_EARLY_SHFL
+        const int sl = c.lin[q];
+#elif !defined(NW_ABL_NOSHFL)
         const int sl = __shfl_up_sync(0xffffffffu, c.send[q], 1);
 #else
         const int sl = c.send[q] + q;                   // ablation: no lane exchange (wrong results)
@@ -315,6 +321,9 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, int4* ring4, u
         up0 = x0; up1 = x1; up2 = x2; up3 = x3;
         d = left[q];
         c.send[q] = live ? x3 : c.send[q];
+#if NW_EARLY_SHFL
+        c.lin[q] = __shfl_up_sync(0xffffffffu, c.send[q], 1);   // next step's left value of row q
+#endif
     }
     c.h[0] = live ? up0 : c.h[0];
     c.h[1] = live ? up1 : c.h[1];
@@ -411,7 +420,7 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
 #pragma unroll
             for (int q = 0; q < CPL; ++q) c.h[q] = 0;
 #pragma unroll
-            for (int q = 0; q < RPS; ++q) c.send[q] = 0;
+            for (int q = 0; q < RPS; ++q) c.send[q] = c.lin[q] = 0;
             c.dprev = 0;
 #if NW_TILED
             if (tl.top_in) {                            // S' of the row above the tile

@@ -1,0 +1,40 @@
+"""A/B the NW kernel template's compile-time knobs at n = 16384 on one B200:
+programs of the default strip layout compiled with different -D settings,
+timed alternately (python scripts/ab_nw.py "NW_EARLY_SHFL=0" "NW_EARLY_SHFL=1")."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2505_08091_b200 import nw, runtime as R  # noqa: E402
+
+n = 16384
+variants = sys.argv[1:] or ["NW_EARLY_SHFL=0", "NW_EARLY_SHFL=1"]
+parts = nw.nw_parts(nw.nw_layout(n), n)
+src, info, _ = nw.program_source(parts)
+progs = []
+for v in variants:
+    head = "".join(f"#define {kv.split('=')[0]} {kv.split('=')[1]}\n" for kv in v.split(",") if kv)
+    progs.append(R.Program(R.compile_cubin(head + src), info, head + src))
+sim = torch.randint(-10, 11, (n, n), device="cuda", dtype=torch.int32)
+outs = [torch.empty(n + 1, n + 1, device="cuda", dtype=torch.int32) for _ in variants]
+
+
+def run(p, o):
+    R.check(R.lib().lego_nw_run(p.handle, sim.data_ptr(), o.data_ptr(), n, 10, 1, R.stream_handle(None)))
+
+
+times = {v: [] for v in variants}
+for rep in range(6):
+    for v, p, o in zip(variants, progs, outs):
+        run(p, o)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(4):
+            run(p, o)
+        b.record()
+        torch.cuda.synchronize()
+        times[v].append(a.elapsed_time(b) / 4 * 1e3)
+for v in variants:
+    t = sorted(times[v])
+    print(f"{v:40s} median {t[len(t) // 2]:8.1f} us  best {t[0]:8.1f} us  equal={torch.equal(outs[0], outs[variants.index(v)])}")
