@@ -81,5 +81,41 @@ for M, N_, Kd in ((256, 256, 128), (200, 136, 72)):
     c = K.gemm(a, b).float()
     ref = a.float() @ b.float().t()
     assert ((c - ref).abs().max() / ref.abs().max()).item() < 1e-2
+# round 2: fill-mode scatters (fused affine windows, fill pass + scatter), the
+# device injectivity gate, the run-walking antidiag inverse, the generated
+# softmax program, NW layout programs (tiled, user orders), a user template
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+for f in (lambda x: 2 * x, lambda x: x * x):
+    gf = L.GroupBy([1 << 12], orders=(L.OrderBy(L.GenP((1 << 12,), L.PermFn(lambda i, f=f: f(i[0]),
+                                                                               lambda i, f=f: f(i[0])), None)),),
+                   injective=True)
+    x = torch.arange(1 << 12, dtype=torch.int32, device="cuda")
+    got = K.remap(x, None, gf, fill=-1).cpu().numpy()
+    want = np.full(got.size, -1, np.int32)
+    want[[f(v) for v in range(1 << 12)]] = np.arange(1 << 12)
+    assert np.array_equal(got, want)
+big = L.GroupBy([1 << 13], orders=(L.OrderBy(L.GenP((1 << 13,), L.PermFn(lambda i: 3 * i[0], lambda i: 3 * i[0]),
+                                                  None)),), injective=True)
+assert K.check_injective(big)
+K.remap(torch.arange(1 << 13, dtype=torch.int16, device="cuda"), None, big)          # gated scatter
+g4 = L.parse_layout("GroupBy([512,512]).OrderBy(GenP([512,512], antidiag))")
+assert np.array_equal(K.inv_map(g4).cpu().numpy(), O.inv_range(O.parse("GroupBy([512,512]).OrderBy(GenP([512,512], antidiag))")))
+x = torch.randn(6, 2048, device="cuda")
+assert np.abs(K.softmax(x).cpu().numpy() - O.softmax_rows_f64(x.cpu().numpy())).max() < 1e-5
+from paper_2505_08091_b200 import nw as NW  # noqa: E402
+from nw_perms import rotate_cells, skew_order, xor_cells  # noqa: E402
+n = 300
+sim = np.random.default_rng(3).integers(-10, 11, size=(n, n), dtype=np.int32)
+for lay in (NW.nw_layout(n, tile_rows=64, tile_order=skew_order(5, 3), cell_order=xor_cells(64)),
+            NW.nw_layout(n, tile_rows=96, tile_order="col", cell_order=rotate_cells(96))):
+    assert np.array_equal(K.nw_score(torch.from_numpy(sim).cuda(), 10, layout=lay).cpu().numpy(), O.nw(sim, 10))
+import ctypes  # noqa: E402
+import test_template as TT  # noqa: E402
+mod = K.compile_template(TT.USER_TEMPLATE, TT.USER_MANIFEST)
+src = torch.arange(256 * 256, dtype=torch.float32, device="cuda")
+dst = torch.empty_like(src)
+mod.launch("lego_tpl_tile", (256,), (256,), [ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr())])
+assert np.array_equal(dst.cpu().numpy(), O.remap(src.cpu().numpy(), None, O.parse(
+    "GroupBy([256,256]).OrderBy(RegP([8,32,8,32],[1,3,2,4]))")))
 torch.cuda.synchronize()
 print("sanitize driver: all checks passed;", len(plans), "remap plans:", sorted(set(p.split(",")[0] for p in plans)))
