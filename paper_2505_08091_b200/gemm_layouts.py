@@ -100,3 +100,40 @@ def grouped_raster_perm(mb: int, nb: int, g: int) -> GenP:
         return Select(head, m_full, full + r2 % tail), Select(head, n_full, r2 // tail)
 
     return GenP((mb, nb), PermFn(fwd, fwd_sym), PermFn(inv, inv_sym), name=None)
+
+
+def operand_strides(layout):
+    """(s_i, s_j) with ``layout.apply((i, j)) == i*s_i + j*s_j`` for every
+    logical (i, j) of a 2-D data layout -- the affine form a single-RegP
+    ``OrderBy`` always has (paper Table I; reference test_acceptance.py:167-208).
+    The tcgen05 GEMM feeds an operand to TMA from exactly these strides, so
+    this is how a LEGO ``Data`` layout (reference matmul workflow,
+    test_acceptance.py:211-234) drives the operand addressing.  Raises
+    ``UnsupportedNode`` for non-affine layouts."""
+    from .errors import UnsupportedNode
+    from .expr import IntConst
+    from .layout import apply_symbolic, index_vars
+    from .simplify import simplify
+    if len(layout.dims) != 2:
+        raise UnsupportedNode("a GEMM operand layout is 2-D")
+    i, j = index_vars(["i", "j"], layout.dims)
+    e = simplify(apply_symbolic(layout, (i, j)))
+    c = layout.apply((0, 0))
+    s_i = layout.apply((1, 0)) - c if layout.dims[0] > 1 else 0
+    s_j = layout.apply((0, 1)) - c if layout.dims[1] > 1 else 0
+    if c != 0 or simplify(e - (i * s_i + j * s_j)) != IntConst(0):
+        raise UnsupportedNode(f"operand layout is not affine (i*{s_i} + j*{s_j}): {layout!r}")
+    return s_i, s_j
+
+
+def operand_major(layout, what: str) -> str:
+    """'row' when the second logical index has stride 1 (row-major storage),
+    'col' when the first has (column-major), for an affine 2-D layout."""
+    from .errors import UnsupportedNode
+    rows, cols = layout.dims
+    s_i, s_j = operand_strides(layout)
+    if (s_i, s_j) == (cols, 1):
+        return "row"
+    if (s_i, s_j) == (1, rows):
+        return "col"
+    raise UnsupportedNode(f"{what}: strides ({s_i}, {s_j}) are neither row- nor column-major")

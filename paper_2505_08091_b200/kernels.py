@@ -1005,14 +1005,36 @@ def gemm_raster(mtiles: int, ntiles: int, batch: int = 1, group: Optional[int] =
     return out
 
 
-def matmul(a, b, *, a_layout: str = "row", b_layout: str = "row", out=None, **kw):
+def matmul(a, b, *, a_layout="row", b_layout="row", out=None, **kw):
     """``C = A @ B`` with ``A`` (M x K) and ``B`` (K x N) given in the Row or Col
     data layout of the paper's four matmul variants: a
     Row operand is stored row-major, a Col operand column-major (i.e. the
     tensor passed holds its transpose, ``A^T`` as (..., K, M) / ``B^T`` as
     (..., N, K)).  Every variant runs as one tcgen05 GEMM; nothing is
-    transposed in memory."""
+    transposed in memory.
+
+    ``a_layout`` / ``b_layout`` may also be LEGO data layouts over the
+    logical (M, K) / (K, N) operand (the reference matmul workflow's
+    ``Data`` layouts, test_acceptance.py:211-234), e.g.
+    ``GroupBy([M,K]).OrderBy(Row(M,K))`` or ``...OrderBy(Col(K,M))``; their
+    affine strides (:func:`.gemm_layouts.operand_strides`) select the TMA
+    operand major, and the tensor passed is the layout's physical buffer."""
+    from . import gemm_layouts as GL
+    if not isinstance(a_layout, str):
+        M, K = a_layout.dims
+        maj = GL.operand_major(a_layout, "A")
+        if a.numel() != M * K:
+            raise ShapeMismatch(f"A holds {a.numel()} elements, its layout {M * K}")
+        a = a.reshape((M, K) if maj == "row" else (K, M))
+        a_layout = maj
+    if not isinstance(b_layout, str):
+        Kb, N = b_layout.dims
+        maj = GL.operand_major(b_layout, "B")
+        if b.numel() != Kb * N:
+            raise ShapeMismatch(f"B holds {b.numel()} elements, its layout {Kb * N}")
+        b = b.reshape((Kb, N) if maj == "row" else (N, Kb))
+        b_layout = maj
     if a_layout not in ("row", "col") or b_layout not in ("row", "col"):
-        raise ShapeMismatch("a_layout / b_layout must be 'row' or 'col'")
+        raise ShapeMismatch("a_layout / b_layout must be 'row', 'col' or a 2-D LEGO layout")
     # gemm computes A @ B'^T with B' = B^T given K-major (N x K) or MN-major (K x N)
     return gemm(a, b, out=out, a_col=a_layout == "col", b_col=b_layout == "row", **kw)

@@ -43,3 +43,45 @@ def test_swizzle_layout_compiles_to_the_device():
     m, k = np.meshgrid(np.arange(128), np.arange(64), indexing="ij")
     want = np.array([hw_sw128_byte(a, b) // 2 for a, b in zip(m.ravel(), k.ravel())])
     assert np.array_equal(got, want)
+
+
+def test_operand_strides_of_data_layouts():
+    """Row / Col data layouts are affine with the strides TMA needs; tiled
+    layouts are not (so they cannot be a tcgen05 operand as is)."""
+    from paper_2505_08091_b200 import gemm_layouts as GL
+    M, K = 256, 128
+    row = L.parse_layout(f"GroupBy([{M},{K}]).OrderBy(Row({M},{K}))")
+    col = L.parse_layout(f"GroupBy([{M},{K}]).OrderBy(Col({K},{M}))")
+    assert GL.operand_strides(row) == (K, 1) and GL.operand_major(row, "A") == "row"
+    assert GL.operand_strides(col) == (1, M) and GL.operand_major(col, "A") == "col"
+    for i, j in ((3, 5), (200, 127), (0, 0)):
+        assert row.apply((i, j)) == i * K + j and col.apply((i, j)) == i + j * M
+    tiled = L.parse_layout(f"GroupBy([{M},{K}]).OrderBy(RegP([8,32,4,32],[1,3,2,4]))")
+    with pytest.raises(L.UnsupportedNode):
+        GL.operand_strides(tiled)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("al,bl", [("row", "row"), ("col", "row"), ("row", "col"), ("col", "col")])
+def test_matmul_with_lego_data_layouts(al, bl):
+    """The four matmul variants driven by LEGO Data layouts equal the string
+    variants and an fp64 reference."""
+    import torch
+    from paper_2505_08091_b200 import kernels as K
+    M, N, Kd = 512, 768, 256
+    la = L.parse_layout(f"GroupBy([{M},{Kd}]).OrderBy({'Row' if al == 'row' else 'Col'}"
+                        f"({M if al == 'row' else Kd},{Kd if al == 'row' else M}))")
+    lb = L.parse_layout(f"GroupBy([{Kd},{N}]).OrderBy({'Row' if bl == 'row' else 'Col'}"
+                        f"({Kd if bl == 'row' else N},{N if bl == 'row' else Kd}))")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(M, Kd, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(Kd, N, device="cuda", generator=g).to(torch.bfloat16)
+    a_buf = A.contiguous().reshape(-1) if al == "row" else A.t().contiguous().reshape(-1)
+    b_buf = B.contiguous().reshape(-1) if bl == "row" else B.t().contiguous().reshape(-1)
+    c = K.matmul(a_buf, b_buf, a_layout=la, b_layout=lb)
+    c2 = K.matmul(a_buf.reshape((M, Kd) if al == "row" else (Kd, M)),
+                  b_buf.reshape((Kd, N) if bl == "row" else (N, Kd)), a_layout=al, b_layout=bl)
+    assert torch.equal(c, c2)
+    ref = A.double() @ B.double()
+    rel = ((c.double() - ref).abs() / ref.abs().clamp_min(1e-2 * ref.abs().max().item())).max().item()
+    assert rel <= 1e-2
