@@ -122,6 +122,9 @@ def dist_setup(args):
         raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
+        # communicator lines (rank count per communicator) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
