@@ -632,3 +632,18 @@ def best_variant(e: Expr, facts: FactSet = EMPTY_FACTS, *, budget: int = DEFAULT
     plain = simplify(e, facts, budget=budget)
     alt = simplify(expand(e), facts, budget=budget, factor_gcd=False)
     return alt if op_count(alt) < op_count(plain) else plain
+
+
+# The paper's Table-II rules one by one, under the reference's names (its
+# tests import them from here); this engine subsumes them (see rules.py).
+from .rules import (  # noqa: E402,F401
+    TABLE_RULES,
+    _Prover,
+    rule_div_below_bound,
+    rule_div_by_one_assoc,
+    rule_div_of_mod,
+    rule_div_of_multiple_sum,
+    rule_mod_below_bound,
+    rule_mod_of_multiple_sum,
+    rule_recompose,
+)
