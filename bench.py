@@ -357,12 +357,19 @@ def run(args):
     kms_each = kernel_event_time(step, max(5, min(args.steps, 20)))
     achieved = 2 * nbytes / (kms * 1e-3) / 1e9
     tr = traffic_table().get("remap_transpose_bf16")
+    # context: a plain device copy of the same 512 MiB on this box, same timing
+    scratch = torch.empty_like(src)
+    copy_ms = time_steps(lambda: scratch.copy_(src), 20, 3, 1) / 20
+    copy_gbs = 2 * nbytes / (copy_ms * 1e-3) / 1e9
+    del scratch
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm"], "unit": "GB/s",
                 "frac": round(achieved / pk["hbm"], 4), "peak_source": pk["source"],
                 "frac_of_8000": round(achieved / 8000.0, 4),
                 "traffic": tr, "algorithmic_bytes_per_launch": 2 * nbytes,
                 "launch_us": round(kms * 1e3, 2),
-                "launch_us_event_bracketed": round(kms_each * 1e3, 2)}
+                "launch_us_event_bracketed": round(kms_each * 1e3, 2),
+                "same_size_copy_gbs": round(copy_gbs, 1),
+                "frac_of_same_size_copy": round(achieved / copy_gbs, 4)}
 
     # e2e: public API with pinned host buffers.  Every step copies its input
     # host->device, remaps, and copies the result device->host.  Consecutive
