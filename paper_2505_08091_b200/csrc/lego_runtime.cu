@@ -235,7 +235,7 @@ extern "C" lego_status lego_program_load(const void* cubin, size_t cubin_len,
             return lego_fail(LEGO_E_ARG, "softmax program lacks its kernels");
         }
     } else if (info->kind == LEGO_PROG_NW) {
-        if (info->smem_bytes != lego_nw_smem_bytes()) {
+        if (info->smem_bytes < lego_nw_smem_bytes()) {
             g_drv.unload(p->mod);
             delete p;
             return lego_fail(LEGO_E_ARG, "NW program shared memory %d != the library's %d", info->smem_bytes,
@@ -441,7 +441,7 @@ extern "C" lego_status lego_nw_run(lego_program p, const int32_t* sim, int32_t* 
     if (n == 0) return LEGO_OK;
     int ni = (int)n;
     void* a2[] = {&sim, &score, &ni, &pp, &pl.H, &pl.nr, &pl.nc, &pl.total, &pl.ticket, &pl.bnd, &pl.top};
-    return launch(p->nw_tiles, pl.ctas, 1, 128, (unsigned)pl.smem, stream, a2);
+    return launch(p->nw_tiles, pl.ctas, 1, 128, (unsigned)p->info.smem_bytes, stream, a2);
 }
 
 static lego_status remap_args(lego_program p, const void* src, void* dst, int64_t batch, int64_t src_stride,

@@ -91,7 +91,10 @@ constexpr int DRAIN = (31 + STEPS - 1) / STEPS;      // extra blocks cover lane 
 constexpr int GRP = NW_GRP;                          // boundary readiness checked every GRP steps
 constexpr int NSLOT = 12;                            // ring blocks
 constexpr int RING_ROWS = NSLOT * BLK;               // 384
-constexpr int BND_ROWS = 256;                        // boundary ring (rows)
+#ifndef NW_BND_ROWS
+#define NW_BND_ROWS 256                              // boundary ring rows (must cover lane 31's lag: 512 for RPS 8)
+#endif
+constexpr int BND_ROWS = NW_BND_ROWS;               // boundary ring (rows)
 constexpr int BND_GROUPS = BND_ROWS / BLK;
 constexpr int ROW_BYTES = STRIP * 4;                 // 512
 constexpr int RING_BYTES = RING_ROWS * ROW_BYTES;    // 192 KiB
@@ -224,6 +227,13 @@ __device__ __forceinline__ void ldsv<2>(u32 a, int (&v)[2]) {
     asm volatile("ld.volatile.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(a));
 }
 template <>
+__device__ __forceinline__ void ldsv<8>(u32 a, int (&v)[8]) {
+    asm volatile("ld.volatile.shared.v4.b32 {%0,%1,%2,%3}, [%8];\n\t"
+                 "ld.volatile.shared.v4.b32 {%4,%5,%6,%7}, [%8+16];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(a));
+}
+template <>
 __device__ __forceinline__ void ldsv<4>(u32 a, int (&v)[4]) {
     asm volatile("ld.volatile.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                  : "r"(a));
@@ -231,7 +241,14 @@ __device__ __forceinline__ void ldsv<4>(u32 a, int (&v)[4]) {
 
 // predicated (branch-free) publication of RPS consecutive boundary words
 __device__ __forceinline__ void publish(int* p, int pred, const int (&v)[RPS]) {
-#if NW_RPS == 4
+#if NW_RPS == 8
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\t"
+        "@q st.relaxed.gpu.global.v4.b32 [%0], {%2, %3, %4, %5};\n\t"
+        "@q st.relaxed.gpu.global.v4.b32 [%0+16], {%6, %7, %8, %9};\n\t}"
+        :: "l"(p), "r"(pred), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),
+           "r"(v[7]) : "memory");
+#elif NW_RPS == 4
     asm volatile(
         "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\t"
         "@q st.relaxed.gpu.global.v4.b32 [%0], {%2, %3, %4, %5};\n\t}"

@@ -14,8 +14,12 @@ parts = nw.nw_parts(nw.nw_layout(n), n)
 src, info, _ = nw.program_source(parts)
 progs = []
 for v in variants:
-    head = "".join(f"#define {kv.split('=')[0]} {kv.split('=')[1]}\n" for kv in v.split(",") if kv)
-    progs.append(R.Program(R.compile_cubin(head + src), info, head + src))
+    kv = dict(x.split("=") for x in v.split(",") if x)
+    head = "".join(f"#define {k} {val}\n" for k, val in kv.items())
+    vi = R.ProgramInfo(kind=info.kind, elem_bytes=4, n=info.n, units=info.units, unit_threads=info.unit_threads,
+                       block=128, smem_bytes=nw.SMEM_BYTES + 4 * (int(kv.get("NW_BND_ROWS", 256)) - 256),
+                       reserved=info.reserved)
+    progs.append(R.Program(R.compile_cubin(head + src), vi, head + src))
 sim = torch.randint(-10, 11, (n, n), device="cuda", dtype=torch.int32)
 outs = [torch.empty(n + 1, n + 1, device="cuda", dtype=torch.int32) for _ in variants]
 
