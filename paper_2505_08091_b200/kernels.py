@@ -875,6 +875,8 @@ def softmax(x, *, out=None, stream=None):
         out = torch.empty_like(x)
     else:
         _check_out(out, tuple(x.shape), torch.float32, x.device, "softmax")
+    if x.numel() == 0:
+        return out
     with torch.cuda.device(x.device):
         st = runtime.stream_handle(stream)
         aligned = (x.data_ptr() | out.data_ptr()) % 16 == 0

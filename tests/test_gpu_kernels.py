@@ -89,6 +89,7 @@ def test_empty_inputs():
     x = torch.empty(0, 64 * 64, device="cuda", dtype=torch.float32)
     assert K.remap(x, None, g).shape == (0, 64 * 64)
     assert K.softmax(torch.empty(0, 8, device="cuda")).shape == (0, 8)
+    assert K.softmax(torch.empty(5, 0, device="cuda")).shape == (5, 0)
     s = K.nw_score(torch.empty(0, 5, 5, device="cuda", dtype=torch.int32), 10)
     assert s.shape == (0, 6, 6)
     s = K.nw_score(torch.empty(0, 0, device="cuda", dtype=torch.int32), 10)
