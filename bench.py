@@ -701,7 +701,11 @@ def other_kernels(args, pk, world):
         sim = torch.randint(-10, 11, (16384, 16384), device="cuda", dtype=torch.int32)
         score = torch.empty(16385, 16385, device="cuda", dtype=torch.int32)
         cells = 16384 * 16384
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from nw_perms import skew_order        # a user-defined GenP (rectangular anti-diagonal order)
         nw_layouts = [("cfg4b_nw_wavefront_i32", NW.nw_layout(16384)),
+                      ("cfg4b_nw_tiles4096_user_skew_i32",
+                       NW.nw_layout(16384, tile_rows=4096, tile_order=skew_order(4, 128))),
                       ("cfg4b_nw_tiles128_antidiag_i32", NW.nw_layout(16384, tile_rows=128, tile_order="antidiag"))]
         for name, lay in nw_layouts:
             K.nw_score(sim, 10, layout=lay, out=score)
