@@ -188,4 +188,6 @@ def nw_test_layouts(n: int):
     if n >= 1024:
         h = n // 8
         out.append((f"tiles{h}+col", nw_layout(n, tile_rows=h, tile_order="col")))
+    if n >= 16384:                                   # the bench's user-ordered layout
+        out.append(("tiles4096+skew", nw_layout(n, tile_rows=4096, tile_order=skew_order(n // 4096, n // 128))))
     return out
