@@ -319,6 +319,60 @@ LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restri
 
 static __device__ __forceinline__ unsigned int lego_word(const lego_v16& v, int i) { return v.w[i]; }
 
+#if LEGO_NARROW
+// Interleave of a digit permutation with one innermost span below a 16-byte
+// vector (lower.narrow_plan; AoS <-> SoA style).  NY = that span, NP = V/NY
+// elements per chunk (a chunk is 16/NY bytes, contiguous on the other side).
+// Mode 1: a thread loads one 16-byte source vector (P x-values x NY) and
+// stores NY chunks, chunk y at gen::map(s + y); mode 2: a thread loads NY
+// chunks, chunk x from gen::map(f + x), and stores one 16-byte vector.  The
+// regrouping of the elements is register-only; every warp access is 32
+// consecutive vectors (mode 1 loads, mode 2 stores) or 32 chunks at P-aligned
+// positions that are contiguous across the lanes that share a run.
+typedef lego_elem<LEGO_ELEM>::t lego_ne;
+#define NY LEGO_NY
+#define NP (LEGO_V / NY)
+template <int B> struct lego_chunk;
+template <> struct lego_chunk<1> { typedef unsigned char t; };
+template <> struct lego_chunk<2> { typedef unsigned short t; };
+template <> struct lego_chunk<4> { typedef unsigned int t; };
+template <> struct lego_chunk<8> { typedef unsigned long long t; };
+typedef lego_chunk<16 / NY>::t lego_ct;
+LEGO_GLOBAL void __launch_bounds__(256) lego_remap(const unsigned char* __restrict__ src,
+                                                   unsigned char* __restrict__ dst,
+                                                   long long src_stride, long long dst_stride) {
+    const unsigned char* s = src + (long long)blockIdx.y * src_stride * LEGO_ELEM;
+    unsigned char* d = dst + (long long)blockIdx.y * dst_stride * LEGO_ELEM;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= gen::N / LEGO_V) return;
+    union { lego_v16 v; lego_ne e[LEGO_V]; } vec;
+    union C { lego_ct c; lego_ne e[NP]; };
+#if LEGO_NARROW == 1
+    vec.v = lego_ld16(s + q * 16);
+#pragma unroll
+    for (int y = 0; y < NY; ++y) {
+        long long pos;
+        gen::map(q * LEGO_V + y, pos);
+        C out;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) out.e[p] = vec.e[p * NY + y];
+        *reinterpret_cast<lego_ct*>(d + pos * LEGO_ELEM) = out.c;
+    }
+#else
+#pragma unroll
+    for (int x = 0; x < NY; ++x) {
+        long long pos;
+        gen::map(q * LEGO_V + x, pos);
+        C in;
+        in.c = __ldg(reinterpret_cast<const lego_ct*>(s + pos * LEGO_ELEM));
+#pragma unroll
+        for (int p = 0; p < NP; ++p) vec.e[p * NY + x] = in.e[p];
+    }
+    lego_st16(d + q * 16, vec.v);
+#endif
+}
+#else
+
 static __device__ __forceinline__ void lego_transpose(const lego_v16 (&in)[LEGO_V], lego_v16 (&out)[LEGO_V]) {
 #if LEGO_ELEM == 4
 #pragma unroll
@@ -500,6 +554,7 @@ LEGO_GLOBAL void __launch_bounds__(LEGO_TBLOCK, LEGO_MINB) lego_remap(const unsi
     }
 }
 #endif  // LEGO_SMEM
+#endif  // LEGO_NARROW
 #endif
 
 // ---------------------------------------------------------------------------

@@ -167,6 +167,8 @@ class RemapPlan:
 
     def __repr__(self):
         names = {1: "gather", 2: "transpose", 3: "band", 4: "scatter", 5: "staged"}
+        if "interleave" in self.detail:
+            names = {**names, 2: "interleave"}
         return (f"RemapPlan({names[self.kind]}, n={self.n_dst}, elem={self.elem_bytes}B, "
                 f"{self.detail})")
 
@@ -231,6 +233,10 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int, route: Optional[Route] =
                                    "LEGO_MINB": TRANSPOSE_MINB, "LEGO_TBLOCK": 32 * warps})
             return RemapPlan(runtime.KIND_TRANSPOSE, n_dst, n_src, elem_bytes, False, False, src,
                              info, f"tile {tp.tx}x{tp.ty} {variant}, SX={tp.sx}, DY={tp.dy}")
+    if not masked and NARROW:
+        npl = lower.narrow_plan(g, f, n_dst, elem_bytes)
+        if npl is not None:
+            return _narrow_remap_plan(npl, n_dst, n_src, elem_bytes)
     width = 1 if masked else lower.contiguous_width(g, f, n_dst, widths=(vec,))
     contig = width >= vec
     if not contig and BOX_STAGING:
@@ -260,6 +266,22 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int, route: Optional[Route] =
                            "LEGO_MASKED": int(masked), "LEGO_UNROLL": unroll})
     return RemapPlan(runtime.KIND_GATHER, n_dst, n_src, elem_bytes, contig, masked, src, info,
                      f"contiguous={contig}, masked={masked}")
+
+
+def _narrow_remap_plan(npl, n_dst, n_src, elem_bytes) -> RemapPlan:
+    """Register interleave for a small innermost span (LEGO_KIND 2,
+    LEGO_NARROW 1/2; lower.narrow_plan)."""
+    vec = 16 // elem_bytes
+    rng = (0, n_dst - 1)
+    body = codegen.constant("N", n_dst) + codegen.generate("map", [npl.var], {"pos": npl.map},
+                                                           bounds={"pos": rng}).source
+    units = (n_dst // vec + 255) // 256
+    info = runtime.ProgramInfo(kind=runtime.KIND_TRANSPOSE, elem_bytes=elem_bytes, n=n_dst, units=units,
+                               unit_threads=1, block=256, smem_bytes=0, reserved=0)
+    src = _assemble(body, {"LEGO_KIND": 2, "LEGO_ELEM": elem_bytes, "LEGO_NARROW": npl.mode, "LEGO_NY": npl.small})
+    side = "source" if npl.mode == 1 else "destination"
+    return RemapPlan(runtime.KIND_TRANSPOSE, n_dst, n_src, elem_bytes, False, False, src, info,
+                     f"interleave: {side}-innermost span {npl.small}, {16 // npl.small}-byte chunks in registers")
 
 
 def _routed_plan(src_layout, dst_layout, elem_bytes, route) -> RemapPlan:
@@ -413,6 +435,8 @@ TRANSPOSE_MINB = int(os.environ.get("LEGO_TRANSPOSE_MINB", "1"))
 TILE_ORDER = os.environ.get("LEGO_TILE_ORDER", "block")
 # CTAs of the persistent transpose variant (2 resident CTAs x 148 SMs by default)
 PERSIST_CTAS = int(os.environ.get("LEGO_PERSIST_CTAS", str(2 * 148)))
+# register interleaves for digit permutations with a small innermost span (0 disables)
+NARROW = int(os.environ.get("LEGO_NARROW", "1"))
 # box-staged gathers (staging.py, LEGO_KIND 5) for non-contiguous gathers whose
 # destination blocks each read one compact source box (0 disables)
 BOX_STAGING = int(os.environ.get("LEGO_BOX", "1"))
@@ -519,7 +543,7 @@ def _remap_program(src_layout, dst_layout, elem_bytes, device: int, route=None, 
     key = ("remap", _layout_key(src_layout), _layout_key(dst_layout), elem_bytes, fill,
            None if route is None else ("route", route.world, route.key), TRANSPOSE_VARIANT,
            BAND_ORDER, PERSIST_CTAS, TILE_ORDER, LOAD_HINT, STORE_HINT, TRANSPOSE_MINB,
-           BAND_ROWS, BAND_DIAGS, BAND_WARPS, TRANSPOSE_WARPS, BOX_STAGING, staging.BOX_TARGET, staging.BOX_STORE,
+           BAND_ROWS, BAND_DIAGS, BAND_WARPS, TRANSPOSE_WARPS, BOX_STAGING, NARROW, staging.BOX_TARGET, staging.BOX_STORE,
            staging.BOX_BULK, staging.BOX_THREADS)
 
     def build():

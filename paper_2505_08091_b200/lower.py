@@ -332,3 +332,68 @@ def value_at(e: Expr, x: Var, v: int) -> Optional[int]:
     """e with x = v, if it folds to a constant."""
     got = simplify(substitute(e, {x.name: IntConst(v)}))
     return got.value if type(got) is IntConst else None
+
+
+class NarrowPlan:
+    """Register interleave of a digit permutation whose innermost digit on one
+    side spans less than a 16-byte vector (AoS <-> SoA style), V = 16/E:
+
+    * mode 1 -- the source-innermost digit y is small (Y | V, Y < V) and the
+      destination-innermost digit x follows it in the source (source stride
+      Y): a lane loads one 16-byte source vector = P = V/Y consecutive x
+      values x Y, and stores Y chunks of P elements, chunk y at destination
+      ``gen::map(s + y)`` (the inverse digit permutation, contiguous in x);
+    * mode 2 -- the destination-innermost digit x is small (Xd | V, Xd < V)
+      and the source-innermost digit y follows it in the destination: a lane
+      loads Xd chunks of P = V/Xd elements, chunk x from source
+      ``gen::map(f + x)`` (the gather map), and stores one 16-byte vector.
+
+    A warp covers 32*V consecutive source (mode 1) / destination (mode 2)
+    elements; ``small`` is Y / Xd."""
+
+    def __init__(self, mode, small, var, fmap):
+        self.mode, self.small, self.var, self.map = mode, small, var, fmap
+
+
+def narrow_plan(g: Expr, f: Var, n: int, elem_bytes: int) -> Optional[NarrowPlan]:
+    """Prove the NarrowPlan conditions on the digit decomposition of g and
+    build the per-chunk address map; None when they do not hold."""
+    if 16 % elem_bytes:
+        return None
+    v = 16 // elem_bytes
+    if n % (32 * v):
+        return None
+    digits = digit_terms(g, f, n)                # (dst lo, span, src stride), dst-innermost first
+    if digits is None or len(digits) < 2:
+        return None
+    x_lo, x_span, sx = digits[0]
+    ydig = [d for d in digits if d[2] == 1]
+    if len(ydig) != 1:
+        return None
+    y_lo, y_span, _ = ydig[0]
+    cand1 = y_span < v and v % y_span == 0 and sx == y_span and x_span % (v // y_span) == 0
+    cand2 = x_span < v and v % x_span == 0 and y_lo == x_span and y_span % (v // x_span) == 0 and sx != 1
+    if cand1 and cand2 and x_span < y_span:
+        cand1 = False                            # prefer the mode with the larger chunks
+    if cand1 and (v // y_span) * elem_bytes < 4:
+        cand1 = False                            # chunks below 4 bytes: not worth it
+    if cand2 and (v // x_span) * elem_bytes < 4:
+        cand2 = False
+    if cand1:
+        mode, small = 1, y_span
+        p = v // small
+        # chunks start at x multiples of P; every other digit keeps them P-aligned in the destination
+        if any(lo % p for lo, span, stride in digits if (lo, span, stride) != digits[0]):
+            return None
+        s = Var("s", VarRange(0, n))
+        h = IntConst(0)                          # inverse digit permutation: destination of source s
+        for lo, span, stride in digits:
+            h = h + ((s // stride) % span) * lo if stride > 1 else h + (s % span) * lo
+        return NarrowPlan(1, small, s, simplify(as_expr(h)))
+    if cand2:
+        mode, small = 2, x_span
+        p = v // small
+        if any(stride % p for lo, span, stride in digits if (lo, span, stride) != ydig[0]):
+            return None
+        return NarrowPlan(2, small, f, g)
+    return None
