@@ -411,6 +411,9 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
         __syncthreads();
         const int t = ctrl->tile;
         if (t >= total) return;
+#ifdef LEGO_NW_DEBUG
+        if (threadIdx.x == 0) g_nw_trace[(blockIdx.x * 4 + 3) * 2048 + 2047] = (unsigned)t + 1;   // tile of this CTA
+#endif
         Tile tl;
         tl.bm = t / tiles_per_matrix;
         tile_of(t - tl.bm * tiles_per_matrix, nc, tl.a, tl.b);

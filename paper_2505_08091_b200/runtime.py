@@ -26,7 +26,7 @@ from .errors import (
 )
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liblego_b200.so")
+LIB_PATH = os.environ.get("LEGO_B200_LIB") or os.path.join(PKG, "liblego_b200.so")   # override: A/B builds
 CACHE_DIR = os.environ.get("LEGO_B200_KCACHE", os.path.join(PKG, "kcache"))
 ARCH = "sm_100a"
 
