@@ -372,56 +372,63 @@ def run(args):
                 "frac_of_same_size_copy": round(achieved / copy_gbs, 4)}
 
     # e2e: public API with pinned host buffers.  Every step copies its input
-    # host->device, remaps, and copies the result device->host.  Consecutive
-    # steps alternate between two streams and buffer sets, so step i+1's H2D
-    # runs while step i's D2H drains (PCIe is full duplex); within a step the
-    # three operations stay ordered on one stream.
-    host_in = [torch.empty(N * N, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
-    host_out = [torch.empty(N * N, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
+    # host->device, remaps, and copies the result device->host, as a three-
+    # stage pipeline over three buffer sets: an H2D stream, the remap stream
+    # and a D2H stream, ordered per step by events, so the two copy engines
+    # stream continuously in both directions (PCIe is full duplex) while each
+    # step's three operations stay ordered.  A buffer set is reused three
+    # steps later, once the remap has read its input and the D2H its output.
+    NB = 3
+    host_in = [torch.empty(N * N, dtype=torch.bfloat16, pin_memory=True) for _ in range(NB)]
+    host_out = [torch.empty(N * N, dtype=torch.bfloat16, pin_memory=True) for _ in range(NB)]
     for h in host_in:
         h.copy_(src)
-    dev_in = [torch.empty_like(src) for _ in range(2)]
-    dev_out = [torch.empty_like(src) for _ in range(2)]
-    streams = [torch.cuda.Stream() for _ in range(2)]
+    dev_in = [torch.empty_like(src) for _ in range(NB)]
+    dev_out = [torch.empty_like(src) for _ in range(NB)]
+    h2d_s, cmp_s, d2h_s = (torch.cuda.Stream() for _ in range(3))
+    ev_in = [torch.cuda.Event() for _ in range(NB)]
+    ev_c = [torch.cuda.Event() for _ in range(NB)]
+    ev_out = [torch.cuda.Event() for _ in range(NB)]
     main = torch.cuda.current_stream()
     e2e_counter = [0]
 
     def e2e_step():
-        k = e2e_counter[0] & 1
+        k = e2e_counter[0]
         e2e_counter[0] += 1
-        s = streams[k]
-        s.wait_stream(main)
-        with torch.cuda.stream(s):
-            dev_in[k].copy_(host_in[k], non_blocking=True)
-            K.remap(dev_in[k], None, layout, out=dev_out[k], stream=s)
-            host_out[k].copy_(dev_out[k], non_blocking=True)
-        main.wait_stream(s)
+        b = k % NB
+        if k >= NB:
+            h2d_s.wait_event(ev_c[b])                   # the remap of step k-NB has read dev_in[b]
+        with torch.cuda.stream(h2d_s):
+            dev_in[b].copy_(host_in[b], non_blocking=True)
+        ev_in[b].record(h2d_s)
+        cmp_s.wait_event(ev_in[b])
+        if k >= NB:
+            cmp_s.wait_event(ev_out[b])                 # the D2H of step k-NB has read dev_out[b]
+        K.remap(dev_in[b], None, layout, out=dev_out[b], stream=cmp_s)
+        ev_c[b].record(cmp_s)
+        d2h_s.wait_stream(cmp_s)
+        with torch.cuda.stream(d2h_s):
+            host_out[b].copy_(dev_out[b], non_blocking=True)
+        ev_out[b].record(d2h_s)
 
     e2e_steps = max(8, args.steps // 4)
 
     def e2e_run():
-        # the two streams overlap each other; main waits on both at the end
         for _ in range(e2e_steps):
-            k = e2e_counter[0] & 1
-            e2e_counter[0] += 1
-            s = streams[k]
-            with torch.cuda.stream(s):
-                dev_in[k].copy_(host_in[k], non_blocking=True)
-                K.remap(dev_in[k], None, layout, out=dev_out[k], stream=s)
-                host_out[k].copy_(dev_out[k], non_blocking=True)
-        for s in streams:
+            e2e_step()
+        for s in (h2d_s, cmp_s, d2h_s):
             main.wait_stream(s)
 
+    for s in (h2d_s, cmp_s, d2h_s):
+        s.wait_stream(main)
     for _ in range(6):
         e2e_step()
     torch.cuda.synchronize()
     barrier(world)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    for s in streams:
-        s.wait_stream(main)
     t0.record(main)
-    for s in streams:
+    for s in (h2d_s, cmp_s, d2h_s):
         s.wait_event(t0)
     e2e_run()
     t1.record(main)
@@ -429,7 +436,7 @@ def run(args):
     e2e_ms = max_over_ranks(t0.elapsed_time(t1), world) / e2e_steps
     # the whole last result, as it arrived in host memory, against the
     # device-timed path's output for the same input (bit-exact, all 2^28 elements)
-    ok_e2e = torch.equal(host_out[(e2e_counter[0] - 1) & 1].cuda(), out)
+    ok_e2e = torch.equal(host_out[(e2e_counter[0] - 1) % NB].cuda(), out)
     e2e_value = world * 2 * nbytes / (e2e_ms * 1e-3) / 1e9
 
     kernels = {}
@@ -459,8 +466,9 @@ def run(args):
                     "d2h_bytes_per_step": nbytes, "steps": e2e_steps,
                     "check": "ok" if ok_e2e else "MISMATCH",
                     "note": "public API kernels.remap; per step H2D of the input from pinned host "
-                            "memory, remap, D2H of the whole result; steps alternate two streams "
-                            "so one step's H2D overlaps the previous step's D2H (PCIe-bound)"},
+                            "memory, remap, D2H of the whole result; a three-stage event pipeline "
+                            "(H2D stream, remap stream, D2H stream, three buffer sets) keeps both "
+                            "copy directions busy (PCIe-bound)"},
             "gpu_launches": launches, "clocks": clocks.summary(), "kernels": kernels,
         }
         print(json.dumps(line), flush=True)

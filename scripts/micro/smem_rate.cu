@@ -6,7 +6,7 @@
 #include <cuda_runtime.h>
 
 template <int MODE>
-__global__ void k(int* out, long long* cyc, int iters) {
+__global__ void k(int* out, long long* cyc, int iters, const int4* __restrict__ g = nullptr) {
     __shared__ int4 buf[64 * 32];
     const int lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) buf[i] = make_int4(i, i ^ 1, i ^ 2, i ^ 3);
@@ -37,6 +37,18 @@ __global__ void k(int* out, long long* cyc, int iters) {
                 asm volatile("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %0, 0;\n\t@q st.shared.v4.b32 [%1], {%2,%3,%4,%5};\n\t}"
                              :: "r"(lane), "r"((unsigned)__cvta_generic_to_shared(&buf[row * 32])), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
             }
+            if (MODE == 13) { int4 w = g[((row + 4 * lane) & 63) * 32 + lane]; acc += w.x ^ w.w; }   // LDG.128 (L1 hits)
+            if (MODE == 14) { int4 w = __ldg(&g[((row + 4 * lane) & 63) * 32 + lane]); acc += w.x ^ w.w; }   // LDG.128.CONSTANT
+            if (MODE == 15 && (u & 3) == 0) {   // step mix with sim from L1: 4 LDG.128 + 4 STS.128 + 4 SHFL
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int r2 = (row + 4 * lane + q) & 63;
+                    int4 w = g[((r2 + 8) & 63) * 32 + lane];
+                    acc += w.x ^ w.w;
+                    buf[r2 * 32 + lane] = v;
+                    acc += __shfl_up_sync(0xffffffffu, v.x + q, 1);
+                }
+            }
             // step-like mixes, per 4 iterations of u (one NW step): 4 LDS.128 + 4 stores + 4 SHFL
             if (MODE >= 8 && (u & 3) == 0) {
 #pragma unroll
@@ -62,10 +74,11 @@ __global__ void k(int* out, long long* cyc, int iters) {
     out[threadIdx.x] = acc + buf[lane].x + v.x;
 }
 
+static int4* g_buf = nullptr;
 template <int MODE>
 double run(int* out, long long* cyc, int warps = 1) {
     const int iters = 20000;
-    k<MODE><<<1, 32 * warps>>>(out, cyc, iters);
+    k<MODE><<<1, 32 * warps>>>(out, cyc, iters, g_buf);
     cudaDeviceSynchronize();
     long long h;
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
@@ -77,11 +90,16 @@ int main() {
     long long* cyc;
     cudaMalloc(&out, 4096);
     cudaMalloc(&cyc, 64);
+    cudaMalloc(&g_buf, 64 * 32 * 16);
+    cudaMemset(g_buf, 1, 64 * 32 * 16);
     for (int w : {1, 2, 4})
         printf("cycles/instr per warp (%d warps): STS.128 %.2f  STS.128 skewed %.2f  STS.64 %.2f  STS.32 %.2f  "
                "LDS.128 dep %.2f  LDS.128 %.2f  LDS.64 %.2f  SHFL %.2f\n", w,
                run<0>(out, cyc, w), run<1>(out, cyc, w), run<2>(out, cyc, w), run<3>(out, cyc, w), run<4>(out, cyc, w),
                run<5>(out, cyc, w), run<6>(out, cyc, w), run<7>(out, cyc, w));
+    for (int rep = 0; rep < 2; ++rep)
+        printf("LDG.128 L1-hit %.2f  LDG.128.nc %.2f cycles/instr; step mix with sim from L1 (4 LDG + 4 STS.128 + 4 SHFL) %.1f\n",
+               run<13>(out, cyc), run<14>(out, cyc), 4 * run<15>(out, cyc));
     printf("1-lane LDS.128 %.2f  1-lane STS.128 %.2f cycles/instr\n", run<11>(out, cyc), run<12>(out, cyc));
     for (int rep = 0; rep < 2; ++rep)
         printf("cycles per NW-like step (1 warp): 4 LDS.128 + 4 STS.128 + 4 SHFL %.1f | + 8 STS.64 instead %.1f | "
