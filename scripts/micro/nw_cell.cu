@@ -31,6 +31,32 @@ __global__ void step_kernel(const int* in, int* out, long long* cyc, int steps) 
         for (int q = 0; q < 4; ++q) { h[q] = __float_as_int(8388608.0f); send[q] = lin[q] = h[q]; }
         d = h[0];
     }
+    __shared__ unsigned tmem_base;
+    unsigned tm = 0;
+    if (V == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;"
+                     :: "r"((unsigned)__cvta_generic_to_shared(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        tm = tmem_base;
+        unsigned w[16];
+        for (int i = 0; i < 16; ++i) w[i] = (unsigned)in[(lane + i) & 255];
+        for (int b = 0; b < 2; ++b)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                         :: "r"(tm + 16 * b), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
+                            "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]),
+                            "r"(w[15]));
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+    }
+    unsigned tv[16];
+    if (V == 5) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=r"(tv[0]), "=r"(tv[1]), "=r"(tv[2]), "=r"(tv[3]), "=r"(tv[4]), "=r"(tv[5]), "=r"(tv[6]), "=r"(tv[7]),
+                       "=r"(tv[8]), "=r"(tv[9]), "=r"(tv[10]), "=r"(tv[11]), "=r"(tv[12]), "=r"(tv[13]), "=r"(tv[14]), "=r"(tv[15])
+                     : "r"(tm));
+    }
     int4 nx1[4], nx2[4];
     for (int q = 0; q < 4; ++q) { nx1[q] = ring[q * 32 + lane]; nx2[q] = ring[(q + 4) * 32 + lane]; }
     long long t0 = clock64();
@@ -39,7 +65,17 @@ __global__ void step_kernel(const int* in, int* out, long long* cyc, int steps) 
 #pragma unroll
     for (int s = s8; s < s8 + 8; ++s) {
         int4 cur[4];
-        if (V == 4) {
+        if (V == 5) {
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            cur[0] = make_int4(tv[0], tv[1], tv[2], tv[3]);
+            cur[1] = make_int4(tv[4], tv[5], tv[6], tv[7]);
+            cur[2] = make_int4(tv[8], tv[9], tv[10], tv[11]);
+            cur[3] = make_int4(tv[12], tv[13], tv[14], tv[15]);
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                         : "=r"(tv[0]), "=r"(tv[1]), "=r"(tv[2]), "=r"(tv[3]), "=r"(tv[4]), "=r"(tv[5]), "=r"(tv[6]), "=r"(tv[7]),
+                           "=r"(tv[8]), "=r"(tv[9]), "=r"(tv[10]), "=r"(tv[11]), "=r"(tv[12]), "=r"(tv[13]), "=r"(tv[14]), "=r"(tv[15])
+                         : "r"(tm + 16 * ((s + 1) & 1)));
+        } else if (V == 4) {
             // two rows per 16-byte load: row q in .x/.y (q even) or .z/.w (q odd)
             const int row = (s * 4 + lane * 4) & 63;
             int4 a, b;
@@ -98,13 +134,21 @@ __global__ void step_kernel(const int* in, int* out, long long* cyc, int steps) 
                 x1 = max(max(__float_as_int(f1), up1), x0);
                 x2 = max(max(__float_as_int(f2), up2), x1);
                 x3 = max(max(__float_as_int(f3), up3), x2);
+            } else if (V == 5) {
+                x0 = max(max(cur[q].x + d + p2, up0), left);
+                x1 = max(max(cur[q].y + up0 + p2, up1), x0);
+                x2 = max(max(cur[q].z + up1 + p2, up2), x1);
+                x3 = max(max(cur[q].w + up2 + p2, up3), x2);
             } else {
                 x0 = max(__viaddmax_s32(d, cur[q].x, up0), left);
                 x1 = max(__viaddmax_s32(up0, cur[q].y, up1), x0);
                 x2 = max(__viaddmax_s32(up1, cur[q].z, up2), x1);
                 x3 = max(__viaddmax_s32(up2, cur[q].w, up3), x2);
             }
-            if (SMEM & 2) ring[((s * 4 + lane * 4 + q + 32) & 63) * 32 + lane] = make_int4(x0, x1, x2, x3);
+            if (SMEM & 4) {   // S' row to tensor memory (lane j's TMEM lane), 4 columns per row
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+                             :: "r"(tm + 32 + 16 * (s & 1) + 4 * q), "r"(x0), "r"(x1), "r"(x2), "r"(x3));
+            } else if (SMEM & 2) ring[((s * 4 + lane * 4 + q + 32) & 63) * 32 + lane] = make_int4(x0, x1, x2, x3);
             up0 = x0; up1 = x1; up2 = x2; up3 = x3;
             d = left;
             send[q] = x3;
@@ -114,6 +158,11 @@ __global__ void step_kernel(const int* in, int* out, long long* cyc, int steps) 
     }
     long long t1 = clock64();
     if (lane == 0) cyc[0] = t1 - t0;
+    if (V == 5) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" :: "r"(tm));
+    }
     __syncwarp();
     out[lane] = h[0] ^ h[1] ^ h[2] ^ h[3] ^ d ^ ring[(lane * 37) & 2047].x ^ ring[(steps + lane) & 2047].w;
 }
@@ -145,6 +194,8 @@ int main() {
                           {run<0, 3>(in, out, cyc, steps), run<1, 3>(in, out, cyc, steps), run<2, 3>(in, out, cyc, steps), run<3, 3>(in, out, cyc, steps), run<4, 3>(in, out, cyc, steps)}};
         for (int m = 0; m < 4; ++m)
             printf("cycles per 4x4 step, %-20s A %.1f  B %.1f  C %.1f  D %.1f  E %.1f\n", names[m], r[m][0], r[m][1], r[m][2], r[m][3], r[m][4]);
+        printf("F (sim from TMEM, tcgen05.ld.32x32b.x16 a step ahead): registers only %.1f, + STS %.1f, + S' by tcgen05.st %.1f\n",
+               run<5, 0>(in, out, cyc, steps), run<5, 2>(in, out, cyc, steps), run<5, 4>(in, out, cyc, steps));
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) printf("err %s\n", cudaGetErrorString(e));

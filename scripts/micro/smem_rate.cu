@@ -6,7 +6,8 @@
 #include <cuda_runtime.h>
 
 template <int MODE>
-__global__ void k(int* out, long long* cyc, int iters, const int4* __restrict__ g = nullptr) {
+__global__ void k(int* out, long long* cyc, int iters, const int4* __restrict__ g = nullptr, int same_smsp = 0) {
+    if (same_smsp && ((threadIdx.x >> 5) & 3)) return;   // only warps 0, 4, 8, ... (SMSP 0) work
     __shared__ int4 buf[64 * 32];
     const int lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) buf[i] = make_int4(i, i ^ 1, i ^ 2, i ^ 3);
@@ -76,9 +77,9 @@ __global__ void k(int* out, long long* cyc, int iters, const int4* __restrict__ 
 
 static int4* g_buf = nullptr;
 template <int MODE>
-double run(int* out, long long* cyc, int warps = 1) {
+double run(int* out, long long* cyc, int warps = 1, int same = 0) {
     const int iters = 20000;
-    k<MODE><<<1, 32 * warps>>>(out, cyc, iters, g_buf);
+    k<MODE><<<1, 32 * warps>>>(out, cyc, iters, g_buf, same);
     cudaDeviceSynchronize();
     long long h;
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
@@ -100,6 +101,9 @@ int main() {
     for (int rep = 0; rep < 2; ++rep)
         printf("LDG.128 L1-hit %.2f  LDG.128.nc %.2f cycles/instr; step mix with sim from L1 (4 LDG + 4 STS.128 + 4 SHFL) %.1f\n",
                run<13>(out, cyc), run<14>(out, cyc), 4 * run<15>(out, cyc));
+    for (int w : {4, 8, 12})
+        printf("same SMSP, %d working warps: STS.128 %.2f  LDS.128 %.2f  SHFL %.2f cycles/instr per warp\n", w / 4 + 1,
+               run<0>(out, cyc, w + 1, 1), run<5>(out, cyc, w + 1, 1), run<7>(out, cyc, w + 1, 1));
     printf("1-lane LDS.128 %.2f  1-lane STS.128 %.2f cycles/instr\n", run<11>(out, cyc), run<12>(out, cyc));
     for (int rep = 0; rep < 2; ++rep)
         printf("cycles per NW-like step (1 warp): 4 LDS.128 + 4 STS.128 + 4 SHFL %.1f | + 8 STS.64 instead %.1f | "
