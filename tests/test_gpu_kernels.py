@@ -74,6 +74,19 @@ def test_nw_vs_c_dp(n):
         np.testing.assert_array_equal(got[b], O.nw(sim[b], 10))
 
 
+@pytest.mark.parametrize("p", [0, -2, 37])
+def test_nw_penalties_and_wide_scores(p):
+    """The library strip kernel with zero, negative and large penalties, and
+    similarities up to +-2^20 (scores near the kernel's +-2^30 contract)."""
+    rng = np.random.default_rng(100 + p)
+    n = 333
+    sim = rng.integers(-(1 << 20), 1 << 20, size=(2, n, n), dtype=np.int32)
+    sim[1] = rng.integers(-3, 4, size=(n, n), dtype=np.int32)
+    got = K.nw_score(torch.from_numpy(sim).cuda(), p).cpu().numpy()
+    for b in range(2):
+        np.testing.assert_array_equal(got[b], O.nw(sim[b], p))
+
+
 def test_nw_16384():
     rng = np.random.default_rng(4)
     n = 16384
