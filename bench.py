@@ -120,7 +120,14 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
-    if world > 1:
+    if world > 1 and os.environ.get("LEGO_BENCH_SHARE_GPU") == "1":
+        # test hook: every rank on cuda:0 with a gloo group, so the multi-rank
+        # control flow (barriers, max over ranks, the JSON line) runs on a
+        # one-GPU box; numbers from such a run are not a scaling measurement
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+    elif world > 1:
         import torch.distributed as dist
         # communicator lines (rank count per communicator) on stderr
         os.environ.setdefault("NCCL_DEBUG", "INFO")
@@ -186,7 +193,8 @@ def max_over_ranks(value, world):
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
