@@ -41,6 +41,12 @@ for text, src_side in (
         ("ExpandBy([30,28],[32,32],GroupBy([32,32]).OrderBy(RegP([2,16,2,16],[1,3,2,4])))", True)):
     for dt in (np.int16, np.int32):
         plans.append(check_remap(text, None, dt, src_side))
+# register interleaves (AoS <-> AoSoA, 1- and 2-byte elements, both directions)
+for text in ("GroupBy([512,32,4]).OrderBy(RegP([512,32,4],[1,3,2]))",
+             "GroupBy([1024,32,2]).OrderBy(RegP([1024,32,2],[1,3,2]))"):
+    for dt in (np.int8, np.int16):
+        for side in (False, True):
+            plans.append(check_remap(text, None, dt, side))
 staging.BOX_BULK = 1
 plans.append(check_remap("GroupBy([256,256]).OrderBy(RegP([4,64,4,64],[1,3,2,4])).OrderBy(RegP([4,4],[2,1]), "
                          "GenP([64,64], antidiag))", None, np.int32))
