@@ -31,14 +31,17 @@
 //
 // Inside a tile (no host loop over diagonals, no grid sync), four warp roles
 // per CTA, one per SM sub-partition:
-//   warp 0  compute:  sweeps the tile anti-diagonally over 4x4 cell blocks --
-//           lane j owns columns 4j..4j+3 and at step s computes rows
-//           4(s-j) .. 4(s-j)+3, i.e. each step is one anti-diagonal of the
-//           (row quads x 32 lane-columns) grid.  The four left values arrive
-//           by one warp shuffle each; everything else is in registers or
-//           16-byte shared loads prefetched two steps ahead;
+//   warp 0  compute:  sweeps the tile in skewed 4x4 cell blocks -- lane j owns
+//           columns 4j..4j+3 and at step s computes rows 4s - SKEW*(j+1) + q,
+//           q = 0..3 (lane j runs SKEW rows behind lane j-1).  With SKEW = 1
+//           row q of lane j takes its left value from row q-1 of lane j-1 in
+//           the same step (one warp shuffle right after that row), so a
+//           strip's 32 lanes are 32 rows apart instead of 32 steps (128 rows)
+//           apart: the horizontal term of the wavefront's critical path
+//           shrinks 4x.  Everything else is in registers or 16-byte shared
+//           loads prefetched two steps ahead;
 //   warp 1  producer: cp.async-stages sim, 32 rows x 128 columns per block,
-//           into a 12-block ring (the compute warp overwrites each sim row
+//           into an 8-block ring (the compute warp overwrites each sim row
 //           with its S' row in place);
 //   warp 2  boundary: polls the left tile's published last column (32-bit
 //           words in global memory, preset to a sentinel no offset score can
@@ -83,26 +86,36 @@ constexpr int BLK = 32;                              // rows per block
 #endif
 constexpr int RPS = NW_RPS;
 constexpr int STEPS = BLK / RPS;                     // compute steps per block
-constexpr int BLAG = (31 + STEPS - 1) / STEPS + 1;   // lane 31 completes block k before block k+BLAG starts
-constexpr int DRAIN = (31 + STEPS - 1) / STEPS;      // extra blocks cover lane 31's 31-step lag
+#ifndef NW_SKEW
+#define NW_SKEW 1                                    // rows each lane runs behind its left neighbour (1, 2 or RPS)
+#endif
+constexpr int SKEW = NW_SKEW;
+static_assert(SKEW >= 1 && SKEW <= RPS && RPS % SKEW == 0, "NW_SKEW must divide NW_RPS");
+constexpr int LAG_BLKS = SKEW;                       // lane 31 runs 32*SKEW rows (SKEW blocks) behind the step's rows
+constexpr int BLAG = LAG_BLKS + 1;                   // lane 31 completes block k before block k+BLAG starts
+constexpr int DRAIN = LAG_BLKS;                      // extra blocks cover lane 31's lag
 #ifndef NW_GRP
-#define NW_GRP (16 / NW_RPS)                         // measured: 4 steps 1068 us, 2 steps 1075, 1 step 1126 (n = 16384)
+#define NW_GRP (16 / NW_RPS)                         // measured: 4 steps 1068 us, 2 steps 1075, 1 step 1126 (n = 16384, SKEW 4)
 #endif
 constexpr int GRP = NW_GRP;                          // boundary readiness checked every GRP steps
-constexpr int NSLOT = 12;                            // ring blocks
-constexpr int RING_ROWS = NSLOT * BLK;               // 384
+#ifndef NW_NSLOT
+#define NW_NSLOT (NW_SKEW == NW_RPS ? 12 : 8)        // lane 31 lags SKEW blocks: SKEW 1 needs fewer ring blocks
+#endif
+constexpr int NSLOT = NW_NSLOT;                      // ring blocks
+constexpr int RING_ROWS = NSLOT * BLK;               // 256 (SKEW 1)
 #ifndef NW_BND_ROWS
 #define NW_BND_ROWS 256                              // boundary ring rows (must cover lane 31's lag: 512 for RPS 8)
 #endif
 constexpr int BND_ROWS = NW_BND_ROWS;               // boundary ring (rows)
 constexpr int BND_GROUPS = BND_ROWS / BLK;
 constexpr int ROW_BYTES = STRIP * 4;                 // 512
-constexpr int RING_BYTES = RING_ROWS * ROW_BYTES;    // 192 KiB
+constexpr int RING_BYTES = RING_ROWS * ROW_BYTES;    // 128 KiB (SKEW 1)
 constexpr int BND_BYTES = BND_ROWS * 4;
 constexpr int MBAR_BYTES = NSLOT * 8;
 constexpr int CTRL_BYTES = 64;
 constexpr int TOP_BYTES = (STRIP + 4) * 4;           // upper tile's bottom row + the corner
 constexpr int SMEM_BYTES = RING_BYTES + BND_BYTES + MBAR_BYTES + CTRL_BYTES + TOP_BYTES;
+#define RING_POW2_PP ((NW_NSLOT & (NW_NSLOT - 1)) == 0)
 #ifndef NW_PRODUCER_NS
 #define NW_PRODUCER_NS 64                            // producer back-off when nothing landed or was issued
 #endif
@@ -207,18 +220,26 @@ __device__ __forceinline__ int slot(int r, int g, int h) {
 
 // compute-warp state: S' of the lane's 4 columns in its last finished row,
 // the diagonal predecessor of its first column, the last-column values it
-// sends right, and sim rows prefetched two steps ahead
-#ifndef NW_EARLY_SHFL
-#define NW_EARLY_SHFL 1          // shuffle each row's last column as soon as it is final (hides SHFL latency)
+// sends right, the shuffled left values, and sim rows prefetched two steps ahead
+#ifndef NW_QFORM
+#define NW_QFORM 1               // left-independent prefix maxima first: one max from the left value to x3
 #endif
 struct Lane {
     int h[CPL];
     int dprev;
     int send[RPS];
-    int lin[RPS];            // NW_EARLY_SHFL: the left neighbour's send[] of the previous step, already shuffled
+    int lin[RPS];            // lin[q]: the left neighbour's x3 of slot q (this step once slot q ran, else the last)
     int4 nx1[RPS], nx2[RPS];
+    u32 o1[RPS], o2[RPS];    // ring byte offsets of the rows in nx1 / nx2 (the S' stores reuse them)
+    u32 lanec;               // -SKEW*(lane+1)*ROW_BYTES + 16*lane: the lane's part of its ring offsets
     int bv[RPS];
 };
+
+__device__ __forceinline__ int max_opaque(int a, int b) {
+    int r;
+    asm("max.s32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
 
 template <int N>
 __device__ __forceinline__ void ldsv(u32 a, int (&v)[N]);
@@ -267,14 +288,16 @@ __device__ __forceinline__ void publish4(int* p, int pred, int x0, int x1, int x
         :: "l"(p), "r"(pred), "r"(x0), "r"(x1), "r"(x2), "r"(x3) : "memory");
 }
 
-__device__ __forceinline__ int ring_wrap(int r) { return r >= RING_ROWS ? r - RING_ROWS : r; }
+constexpr bool RING_POW2 = (RING_ROWS & (RING_ROWS - 1)) == 0;
 __device__ __forceinline__ int ring_mod(int r) {
+    if (RING_POW2) return r & (RING_ROWS - 1);
     int m = r % RING_ROWS;
     return m < 0 ? m + RING_ROWS : m;
 }
-// the int4 cell of lane group `lane` in ring row rm (tile row r)
-__device__ __forceinline__ int4* ring_cell(int4* ring4, int rm, int r, int lane, int h) {
-    return ring4 + (rm << 5) + slot(r, lane, h);
+// ring byte offset of lane group g's 16 bytes (columns 4g..4g+3) of tile row
+// r: ring row r mod RING_ROWS, 16-byte slot slot(r, g)
+__device__ __forceinline__ u32 cell_off(int r, int g, int h) {
+    return (u32)(ring_mod(r) * ROW_BYTES + 16 * slot(r, g, h));
 }
 
 // Tile geometry shared by the roles.
@@ -289,82 +312,97 @@ struct Tile {
     int* top_out;    // tiled: where this tile publishes its bottom row, or null
 };
 
-// one anti-diagonal step of the compute warp: lane j computes the RPS x 4
-// block rows r0 = RPS(s-j) .. r0+RPS-1 (tile rows), columns 4j..4j+3 of the tile
-// rm = r0 mod RING_ROWS (RPS | RING_ROWS, so rows r0 .. r0+RPS-1 never straddle the wrap)
+// one step of the compute warp: lane j computes the RPS x 4 block of tile rows
+// r0 = RPS*s - SKEW*(j+1) .. r0+RPS-1, columns 4j..4j+3 of the tile.  Row q's
+// left value is lane j-1's last column of its slot q-SKEW: from this step when
+// q >= SKEW, else from the previous one.
 template <bool GUARD>
-__device__ __forceinline__ void nw_step(Lane& c, int s, int lane, int4* ring4, u32 bnd, int p2, const Tile& tl,
-                                        int h, int* pub_row, int rm) {
-    const int r0 = RPS * (s - lane);
-    const int rmp = ring_wrap(rm + 2 * RPS);
+__device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char* ring, u32 bnd, int p2, const Tile& tl,
+                                        int h, int* pub_row) {
+    const int r0 = RPS * s - SKEW * (lane + 1);
     int4 cur[RPS];
+    u32 so[RPS];
     int lb[RPS];
 #pragma unroll
     for (int q = 0; q < RPS; ++q) {
         cur[q] = c.nx1[q];
+        so[q] = c.o1[q];
         c.nx1[q] = c.nx2[q];
+        c.o1[q] = c.o2[q];
+#if NW_GEN_SLOTS || !RING_POW2_PP
+        c.o2[q] = cell_off(r0 + 2 * RPS + q, lane, h);
+#else
+        // (r mod RING_ROWS) * ROW_BYTES + 16*lane with one add and one mask:
+        // 16*lane < ROW_BYTES and RING_BYTES divides 2^32
+        c.o2[q] = ((u32)(s + 2) * (u32)(RPS * ROW_BYTES) + c.lanec + (u32)(q * ROW_BYTES)) & (u32)(RING_BYTES - 1);
+#endif
 #ifndef NW_ABL_NOLDS
-        c.nx2[q] = *ring_cell(ring4, rmp + q, r0 + 2 * RPS + q, lane, h);
+        c.nx2[q] = *reinterpret_cast<const int4*>(ring + c.o2[q]);
 #else
         c.nx2[q] = make_int4(q, lane, s, q ^ lane);
 #endif
         lb[q] = c.bv[q];
     }
     ldsv<RPS>(bnd + (u32)(((RPS * (s + 1)) & (BND_ROWS - 1)) * 4), c.bv);   // next step's boundary
-    int left[RPS];
-#pragma unroll
-    for (int q = 0; q < RPS; ++q) {
-#if NW_EARLY_SHFL
-        const int sl = c.lin[q];
-#elif !defined(NW_ABL_NOSHFL)
-        const int sl = __shfl_up_sync(0xffffffffu, c.send[q], 1);
-#else
-        const int sl = c.send[q] + q;                   // ablation: no lane exchange (wrong results)
-#endif
-        left[q] = lane == 0 ? lb[q] : sl;
-    }
-    const bool live = !GUARD || r0 >= 0;                // lanes start one step apart
     int up0 = c.h[0], up1 = c.h[1], up2 = c.h[2], up3 = c.h[3];
     int d = c.dprev;
 #pragma unroll
     for (int q = 0; q < RPS; ++q) {
-        const int x0 = max(max(cur[q].x + d + p2, up0), left[q]);
+        const int left = lane == 0 ? lb[q] : c.lin[(q + RPS - SKEW) % RPS];
+        const bool live = !GUARD || r0 + q >= 0;        // lanes start SKEW rows apart
+#if NW_QFORM
+        // prefix maxima of the row without its left value; x_c = max(Q_c, left).
+        // The final maxima are opaque (asm) so the compiler cannot re-associate
+        // them back into the 4-deep chain from `left`: left -> x3 is one op.
+        const int q0 = max(cur[q].x + d + p2, up0);
+        const int q1 = max(max(cur[q].y + up0 + p2, up1), q0);
+        const int q2 = max(max(cur[q].z + up1 + p2, up2), q1);
+        const int q3 = max(max(cur[q].w + up2 + p2, up3), q2);
+        const int x3 = max_opaque(q3, left);
+        c.lin[q] = __shfl_up_sync(0xffffffffu, x3, 1);
+        const int x0 = max_opaque(q0, left);
+        const int x1 = max_opaque(q1, left);
+        const int x2 = max_opaque(q2, left);
+#else
+        const int x0 = max(max(cur[q].x + d + p2, up0), left);
         const int x1 = max(max(cur[q].y + up0 + p2, up1), x0);
         const int x2 = max(max(cur[q].z + up1 + p2, up2), x1);
         const int x3 = max(max(cur[q].w + up2 + p2, up3), x2);
-#ifndef NW_ABL_NOSTS
-        if (live) *ring_cell(ring4, rm + q, r0 + q, lane, h) = make_int4(x0, x1, x2, x3);   // S' replaces sim in place
+        c.lin[q] = __shfl_up_sync(0xffffffffu, x3, 1);
 #endif
-        up0 = x0; up1 = x1; up2 = x2; up3 = x3;
-        d = left[q];
-        c.send[q] = live ? x3 : c.send[q];
-#if NW_EARLY_SHFL
-        c.lin[q] = __shfl_up_sync(0xffffffffu, c.send[q], 1);   // next step's left value of row q
+#ifndef NW_ABL_NOSTS
+        if (live) *reinterpret_cast<int4*>(ring + so[q]) = make_int4(x0, x1, x2, x3);   // S' replaces sim in place
+#endif
+        up0 = live ? x0 : up0;
+        up1 = live ? x1 : up1;
+        up2 = live ? x2 : up2;
+        up3 = live ? x3 : up3;
+        d = live ? left : d;
+        c.send[q] = x3;
+#if NW_TILED
+        // the tile's last row goes to the tile below (every lane, its 4 columns)
+        publish4(tl.top_out + 4 * lane, (tl.top_out != nullptr) & (r0 + q == tl.rows - 1), x0, x1, x2, x3);
 #endif
     }
-    c.h[0] = live ? up0 : c.h[0];
-    c.h[1] = live ? up1 : c.h[1];
-    c.h[2] = live ? up2 : c.h[2];
-    c.h[3] = live ? up3 : c.h[3];
-    c.dprev = live ? d : c.dprev;
-    // the tile's last column goes to the right neighbour (lane 31, rows of the tile)
-    const int pub = (lane == 31) & (r0 < tl.rows) & live;
+    c.h[0] = up0;
+    c.h[1] = up1;
+    c.h[2] = up2;
+    c.h[3] = up3;
+    c.dprev = d;
+    // the tile's last column goes to the right neighbour (lane 31: r0 is a
+    // multiple of 4, so its RPS rows are all live or all not)
+    const int pub = (lane == 31) & (r0 >= 0) & (r0 < tl.rows);
 #ifndef NW_ABL_NOPUB
     publish(pub_row, pub, c.send);
 #endif
-#if NW_TILED
-    // the tile's last row goes to the tile below (every lane, its 4 columns)
-    publish4(tl.top_out + 4 * lane, (tl.top_out != nullptr) & (r0 + RPS == tl.rows), up0, up1, up2, up3);
-#endif
 }
 
-// one block of STEPS steps (32 rows of lane 0); boundary readiness is checked
-// every GRP steps against a counter value prefetched GRP steps earlier
+// one block of STEPS steps (lane 0's rows 32k - SKEW ..); boundary readiness is
+// checked every GRP steps against a counter value prefetched GRP steps earlier
 template <bool GUARD>
-__device__ __forceinline__ void nw_block(Lane& c, int k, int lane, int4* ring4, u32 bnd, int p2, const Tile& tl,
+__device__ __forceinline__ void nw_block(Lane& c, int k, int lane, unsigned char* ring, u32 bnd, int p2, const Tile& tl,
                                          int h, int& rd, const int* ready, int rows_total) {
-    int* pub_blk = tl.my_bnd + tl.row0 + RPS * (k * STEPS - lane);  // lane 31's rows of step u: + RPS*u
-    int rm = ring_mod(k * BLK - RPS * lane);
+    int* pub_blk = tl.my_bnd + tl.row0 + k * BLK - 32 * SKEW;  // lane 31's rows of step u: + RPS*u
 #pragma unroll
     for (int u = 0; u < STEPS; ++u) {
         const int s = k * STEPS + u;
@@ -373,8 +411,7 @@ __device__ __forceinline__ void nw_block(Lane& c, int k, int lane, int4* ring4, 
             while (rd < need) rd = ldv(ready);
             rd = ldv(ready);
         }
-        nw_step<GUARD>(c, s, lane, ring4, bnd, p2, tl, h, pub_blk + RPS * u, rm);
-        rm = ring_wrap(rm + RPS);
+        nw_step<GUARD>(c, s, lane, ring, bnd, p2, tl, h, pub_blk + RPS * u);
     }
 }
 
@@ -451,7 +488,7 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
             }
 #endif
             const int p2 = 2 * p;
-            int4* ring4 = reinterpret_cast<int4*>(smem);
+            c.lanec = (u32)(16 * lane) - (u32)(SKEW * (lane + 1) * ROW_BYTES);
             int pl = ldv(&ctrl->loaded);
             int rd = ldv(&ctrl->ready);
             for (int k = 0; k < tl.nblocks + DRAIN; ++k) {
@@ -463,20 +500,23 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
                 // the last steps of block k prefetch block k+1's first rows: need both
                 const int need_blk = min(k + 1, tl.nblocks + DRAIN - 1);
                 while (pl < need_blk) pl = ldv(&ctrl->loaded);
+                if (lane == 0) NW_TRACE(0, 1024 + k);      // operands in
                 if (k == 0) {                           // operands of the first two steps
                     while (rd < RPS) rd = ldv(&ctrl->ready);
 #pragma unroll
                     for (int q = 0; q < RPS; ++q) {
-                        c.nx1[q] = *ring_cell(ring4, ring_mod(-RPS * lane + q), -RPS * lane + q, lane, H);
-                        c.nx2[q] = *ring_cell(ring4, ring_mod(RPS - RPS * lane + q), RPS - RPS * lane + q, lane, H);
+                        c.o1[q] = cell_off(q - SKEW * (lane + 1), lane, H);
+                        c.o2[q] = cell_off(RPS + q - SKEW * (lane + 1), lane, H);
+                        c.nx1[q] = *reinterpret_cast<const int4*>(smem + c.o1[q]);
+                        c.nx2[q] = *reinterpret_cast<const int4*>(smem + c.o2[q]);
                     }
                     ldsv<RPS>(bnd, c.bv);
                 }
                 pl = ldv(&ctrl->loaded);                // prefetch for the next block
-                if (k < (31 + STEPS - 1) / STEPS)
-                    nw_block<true>(c, k, lane, ring4, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
+                if (k < LAG_BLKS)                       // lane 31's first rows are negative
+                    nw_block<true>(c, k, lane, smem, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
                 else
-                    nw_block<false>(c, k, lane, ring4, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
+                    nw_block<false>(c, k, lane, smem, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
             }
             __syncwarp();
             if (lane == 0) stv(&ctrl->computed, tl.nblocks + DRAIN - 1);
@@ -519,6 +559,7 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
                             }
                         }
                         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(mb) : "memory");
+                        if (lane == 0) NW_TRACE(1, 1024 + k);  // block issued
                     } else {
                         asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}"
                                      :: "r"(mb) : "memory");
@@ -579,7 +620,9 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
 #endif
             // Lane l polls row 32m + l of the left column; rows are handed to
             // the compute warp in order through ctrl->ready as soon as a
-            // prefix of the group is in.
+            // prefix of the group is in.  Row r sits at ring index r + SKEW,
+            // so lane 0's rows 4s - SKEW .. 4s - SKEW + 3 are one aligned
+            // 16-byte load.
             const int* left = tl.my_bnd - n_pad + tl.row0;
             const int groups = tl.nblocks + DRAIN;
             for (int m = 0; m < groups; ++m) {
@@ -599,7 +642,7 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
                     const unsigned ball = __ballot_sync(0xffffffffu, ok);
                     const int tt = ball == 0xffffffffu ? 32 : __ffs(~ball) - 1;   // ready prefix
                     if (ok && !written && lane < tt) {
-                        asm volatile("st.shared.b32 [%0], %1;" :: "r"(bnd + (u32)((r & (BND_ROWS - 1)) * 4)),
+                        asm volatile("st.shared.b32 [%0], %1;" :: "r"(bnd + (u32)(((r + SKEW) & (BND_ROWS - 1)) * 4)),
                                      "r"(v) : "memory");
                         written = true;
                     }
@@ -626,7 +669,11 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
             for (int q = 0; q < CPL; ++q) ok[q] = tl.col0 + 32 * q + lane < n;
             for (int k = 0; k < tl.nblocks; ++k) {
                 while (ldv_acq(&ctrl->computed) < k) __nanosleep(NW_FLUSHER_NS);
+                if (lane == 0) NW_TRACE(3, 1024 + k);      // block computed: flush starts
                 const int rows = min(BLK, tl.rows - k * BLK);
+#ifdef NW_ABL_NOFLUSH
+                if (rows > 0) { __syncwarp(); if (lane == 0) stv(&ctrl->flushed, k); continue; }   // ablation: no output
+#endif
                 const int* src = ring_gen + (k % NSLOT) * BLK * STRIP;
                 int* dst = sc + (long long)(tl.row0 + k * BLK + 1) * ld + tl.col0 + 1 + lane;
                 int off = (tl.row0 + k * BLK + tl.col0 + lane + 2) * p;   // (i + j) * p of column lane, row k*BLK

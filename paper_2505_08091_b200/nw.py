@@ -51,8 +51,15 @@ from .layout import GenP, GroupBy, OrderBy, RegP, resolve_builtin_perm
 STRIP = 128                       # columns per tile (32 lanes x 4 columns)
 LANES = 32
 BLK = 32                          # rows per staging block
-# nw_kernels.cuh SMEM_BYTES: 384-row ring + boundary ring + mbarriers + control + top row
-SMEM_BYTES = 384 * STRIP * 4 + 256 * 4 + 12 * 8 + 64 + (STRIP + 4) * 4
+# nw_kernels.cuh SMEM_BYTES: 256-row ring (8 blocks) + boundary ring + mbarriers + control + top row
+NSLOT = 8
+
+
+def smem_bytes(nslot: int = NSLOT, bnd_rows: int = 256) -> int:
+    return nslot * 32 * STRIP * 4 + bnd_rows * 4 + nslot * 8 + 64 + (STRIP + 4) * 4
+
+
+SMEM_BYTES = smem_bytes()
 KIND_NW = 6
 
 

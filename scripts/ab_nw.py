@@ -17,7 +17,9 @@ for v in variants:
     kv = dict(x.split("=") for x in v.split(",") if x)
     head = "".join(f"#define {k} {val}\n" for k, val in kv.items())
     vi = R.ProgramInfo(kind=info.kind, elem_bytes=4, n=info.n, units=info.units, unit_threads=info.unit_threads,
-                       block=128, smem_bytes=nw.SMEM_BYTES + 4 * (int(kv.get("NW_BND_ROWS", 256)) - 256),
+                       block=128,
+                       smem_bytes=max(nw.SMEM_BYTES, nw.smem_bytes(int(kv.get("NW_NSLOT", 12 if kv.get("NW_SKEW") == "4" else 8)),
+                                                                   int(kv.get("NW_BND_ROWS", 256)))),
                        reserved=info.reserved)
     progs.append(R.Program(R.compile_cubin(head + src), vi, head + src))
 sim = torch.randint(-10, 11, (n, n), device="cuda", dtype=torch.int32)
