@@ -95,7 +95,7 @@ constexpr int LAG_BLKS = SKEW;                       // lane 31 runs 32*SKEW row
 constexpr int BLAG = LAG_BLKS + 1;                   // lane 31 completes block k before block k+BLAG starts
 constexpr int DRAIN = LAG_BLKS;                      // extra blocks cover lane 31's lag
 #ifndef NW_GRP
-#define NW_GRP (16 / NW_RPS)                         // measured: 4 steps 1068 us, 2 steps 1075, 1 step 1126 (n = 16384, SKEW 4)
+#define NW_GRP 2                                     // measured (n = 16384, SKEW 1): 1 step 912 us, 2 steps 882, 4 steps 897
 #endif
 constexpr int GRP = NW_GRP;                          // boundary readiness checked every GRP steps
 #ifndef NW_NSLOT
@@ -221,6 +221,9 @@ __device__ __forceinline__ int slot(int r, int g, int h) {
 // compute-warp state: S' of the lane's 4 columns in its last finished row,
 // the diagonal predecessor of its first column, the last-column values it
 // sends right, the shuffled left values, and sim rows prefetched two steps ahead
+#ifndef NW_ORDERED
+#define NW_ORDERED 1             // shuffle, S' store and prefetch of each slot issued in order (volatile asm)
+#endif
 #ifndef NW_QFORM
 #define NW_QFORM 1               // left-independent prefix maxima first: one max from the left value to x3
 #endif
@@ -323,6 +326,7 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char*
     int4 cur[RPS];
     u32 so[RPS];
     int lb[RPS];
+    const u32 ringa = static_cast<u32>(__cvta_generic_to_shared(ring));
 #pragma unroll
     for (int q = 0; q < RPS; ++q) {
         cur[q] = c.nx1[q];
@@ -336,10 +340,12 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char*
         // 16*lane < ROW_BYTES and RING_BYTES divides 2^32
         c.o2[q] = ((u32)(s + 2) * (u32)(RPS * ROW_BYTES) + c.lanec + (u32)(q * ROW_BYTES)) & (u32)(RING_BYTES - 1);
 #endif
+#if !NW_ORDERED
 #ifndef NW_ABL_NOLDS
         c.nx2[q] = *reinterpret_cast<const int4*>(ring + c.o2[q]);
 #else
         c.nx2[q] = make_int4(q, lane, s, q ^ lane);
+#endif
 #endif
         lb[q] = c.bv[q];
     }
@@ -348,7 +354,11 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char*
     int d = c.dprev;
 #pragma unroll
     for (int q = 0; q < RPS; ++q) {
+#ifndef NW_ABL_LATESHFL
         const int left = lane == 0 ? lb[q] : c.lin[(q + RPS - SKEW) % RPS];
+#else
+        const int left = lane == 0 ? lb[q] : c.lin[q];   // ablation: last step's shuffle (wrong results)
+#endif
         const bool live = !GUARD || r0 + q >= 0;        // lanes start SKEW rows apart
 #if NW_QFORM
         // prefix maxima of the row without its left value; x_c = max(Q_c, left).
@@ -359,7 +369,11 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char*
         const int q2 = max(max(cur[q].z + up1 + p2, up2), q1);
         const int q3 = max(max(cur[q].w + up2 + p2, up3), q2);
         const int x3 = max_opaque(q3, left);
+#if NW_ORDERED
+        asm volatile("shfl.sync.up.b32 %0, %1, 1, 0, 0xffffffff;" : "=r"(c.lin[q]) : "r"(x3));
+#else
         c.lin[q] = __shfl_up_sync(0xffffffffu, x3, 1);
+#endif
         const int x0 = max_opaque(q0, left);
         const int x1 = max_opaque(q1, left);
         const int x2 = max_opaque(q2, left);
@@ -370,7 +384,17 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char*
         const int x3 = max(max(cur[q].w + up2 + p2, up3), x2);
         c.lin[q] = __shfl_up_sync(0xffffffffu, x3, 1);
 #endif
-#ifndef NW_ABL_NOSTS
+#if NW_ORDERED
+        // the slot's shared-memory traffic right behind its shuffle, in
+        // program order (volatile asm): the next slot's shuffle does not queue
+        // behind a burst of 128-bit stores and loads
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t"
+                     "@p st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n\t}"
+                     :: "r"(ringa + so[q]), "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"((u32)live) : "memory");
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(c.nx2[q].x), "=r"(c.nx2[q].y), "=r"(c.nx2[q].z), "=r"(c.nx2[q].w)
+                     : "r"(ringa + c.o2[q]) : "memory");
+#elif !defined(NW_ABL_NOSTS)
         if (live) *reinterpret_cast<int4*>(ring + so[q]) = make_int4(x0, x1, x2, x3);   // S' replaces sim in place
 #endif
         up0 = live ? x0 : up0;
@@ -395,6 +419,9 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char*
 #ifndef NW_ABL_NOPUB
     publish(pub_row, pub, c.send);
 #endif
+#ifdef LEGO_NW_DEBUG
+    if (pub && r0 < 512) NW_TRACE(3, 1536 + r0 / 4);   // lane 31 published rows r0..r0+3
+#endif
 }
 
 // one block of STEPS steps (lane 0's rows 32k - SKEW ..); boundary readiness is
@@ -410,6 +437,7 @@ __device__ __forceinline__ void nw_block(Lane& c, int k, int lane, unsigned char
             const int need = min(RPS * (s + GRP + 1), rows_total);   // the helper stops at rows_total
             while (rd < need) rd = ldv(ready);
             rd = ldv(ready);
+            if (lane == 0 && s < 512) NW_TRACE(0, 1536 + s);   // readiness check passed
         }
         nw_step<GUARD>(c, s, lane, ring, bnd, p2, tl, h, pub_blk + RPS * u);
     }
@@ -649,6 +677,10 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
                     if (tt > told) {
                         __syncwarp();
                         if (lane == 0) stv(&ctrl->ready, m * BLK + tt);
+#ifdef LEGO_NW_DEBUG
+                        if (lane == 0 && m * BLK + tt <= 512)      // time row (m*BLK + tt - 1) became ready
+                            for (int x = m * BLK + told; x < m * BLK + tt; ++x) NW_TRACE(2, 1024 + x);
+#endif
                         told = tt;
                     }
                     if (tt == 32) break;

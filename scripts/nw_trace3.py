@@ -48,3 +48,18 @@ for w in (0, 64, 127):
           f"flush work {med(f_done - f_start)}, flush start - computed publication {med(f_start - T[0, ks + 2]) if False else ''}")
     print(f"   flush start(k) - compute start(k+BLAG=2) {med(f_start - T[0, ks + 2])}, (k+5) {med(f_start - T[0, ks + 5])};"
           f" issue(k) - flush done(k-12) {med(T[1, 1024 + ks] - T[3, ks - 12])}, (k-8) {med(T[1, 1024 + ks] - T[3, ks - 8])}")
+print()
+# strip w's lane 31 finishes rows 32m..32m+31 in its last step of compute block m + SKEW
+# (~ compute start of block m + SKEW + 1); strip w+1's boundary warp has handed the
+# whole group once its lane 31 logs group m
+skew = int(os.environ.get("NW_SKEW", "1"))
+hs = []
+for w in range(1, 127):
+    cw, cn = strip_of[w], strip_of[w + 1]
+    Tw, Tn = (a[cw] - t0) / 1000.0, (a[cn] - t0) / 1000.0
+    hs.append(np.median(Tn[2, ks] - Tw[0, ks + skew + 1]))
+    if w in (1, 64, 126):
+        need = Tn[0, ks] - Tn[2, ks]
+        print(f"strip {w}->{w + 1}: group m handed - producer strip's compute start(m+{skew + 1}) median {hs[-1] * 1000:.0f} ns;"
+              f" consumer compute start(k) - its boundary group k handed {np.median(need) * 1000:.0f} ns")
+print(f"hand-off latency over strips: median {np.median(hs) * 1000:.0f} ns, mean {np.mean(hs) * 1000:.0f}")
