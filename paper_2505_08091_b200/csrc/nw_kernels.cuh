@@ -359,7 +359,9 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char*
 #else
         const int left = lane == 0 ? lb[q] : c.lin[q];   // ablation: last step's shuffle (wrong results)
 #endif
-        const bool live = !GUARD || r0 + q >= 0;        // lanes start SKEW rows apart
+        // lanes start SKEW rows apart; tiled: a lane stops at the tile's last
+        // row, so its state ends on the bottom row published below the tile
+        const bool live = !GUARD || (r0 + q >= 0 && (!NW_TILED || r0 + q < tl.rows));
 #if NW_QFORM
         // prefix maxima of the row without its left value; x_c = max(Q_c, left).
         // The final maxima are opaque (asm) so the compiler cannot re-associate
@@ -403,10 +405,6 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char*
         up3 = live ? x3 : up3;
         d = live ? left : d;
         c.send[q] = x3;
-#if NW_TILED
-        // the tile's last row goes to the tile below (every lane, its 4 columns)
-        publish4(tl.top_out + 4 * lane, (tl.top_out != nullptr) & (r0 + q == tl.rows - 1), x0, x1, x2, x3);
-#endif
     }
     c.h[0] = up0;
     c.h[1] = up1;
@@ -541,11 +539,15 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
                     ldsv<RPS>(bnd, c.bv);
                 }
                 pl = ldv(&ctrl->loaded);                // prefetch for the next block
-                if (k < LAG_BLKS)                       // lane 31's first rows are negative
+                if (k < LAG_BLKS || (NW_TILED && k + 1 >= tl.nblocks))   // lane 31's first rows are negative; tiled: rows past the tile
                     nw_block<true>(c, k, lane, smem, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
                 else
                     nw_block<false>(c, k, lane, smem, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
             }
+#if NW_TILED
+            // the tile's last row (each lane's state stopped there) goes to the tile below
+            publish4(tl.top_out + 4 * lane, tl.top_out != nullptr, c.h[0], c.h[1], c.h[2], c.h[3]);
+#endif
             __syncwarp();
             if (lane == 0) stv(&ctrl->computed, tl.nblocks + DRAIN - 1);
         } else if (warp == 1) {

@@ -10,7 +10,17 @@ from paper_2505_08091_b200 import nw, runtime as R  # noqa: E402
 
 n = 16384
 variants = sys.argv[1:] or ["NW_EARLY_SHFL=0", "NW_EARLY_SHFL=1"]
-parts = nw.nw_parts(nw.nw_layout(n), n)
+# NW_AB_LAYOUT=tiles4096 / tiles128: the bench's tiled layouts (default: strips)
+_which = __import__("os").environ.get("NW_AB_LAYOUT", "strips")
+if _which == "tiles4096":
+    sys.path.insert(0, "tests")
+    from nw_perms import skew_order
+    _lay = nw.nw_layout(n, tile_rows=4096, tile_order=skew_order(4, 128))
+elif _which == "tiles128":
+    _lay = nw.nw_layout(n, tile_rows=128, tile_order="antidiag")
+else:
+    _lay = nw.nw_layout(n)
+parts = nw.nw_parts(_lay, n)
 src, info, _ = nw.program_source(parts)
 progs = []
 for v in variants:
