@@ -87,6 +87,17 @@ def test_nw_penalties_and_wide_scores(p):
         np.testing.assert_array_equal(got[b], O.nw(sim[b], p))
 
 
+def test_nw_strips_more_than_ctas():
+    """158 strips on 148 persistent CTAs: CTAs claim a second strip (ticket
+    order across the batch), n not a multiple of 4 (scalar sim staging)."""
+    rng = np.random.default_rng(9)
+    n = 10001
+    sim = rng.integers(-10, 11, size=(2, n, n), dtype=np.int32)
+    got = K.nw_score(torch.from_numpy(sim).cuda(), 7).cpu().numpy()
+    for b in range(2):
+        np.testing.assert_array_equal(got[b], O.nw(sim[b], 7))
+
+
 def test_nw_16384():
     rng = np.random.default_rng(4)
     n = 16384
