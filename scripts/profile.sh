@@ -10,7 +10,7 @@ for k in transpose gather band softmax gemm nw apply_map; do
   case $k in
     gemm) pat="regex:gemm_bf16";;
     softmax) pat="regex:softmax_rows";;
-    nw) pat="regex:nw_strips";;
+    nw) pat="regex:lego_nw_tiles";;
     apply_map) pat="regex:lego_inv_map";;
     *) pat="regex:lego_remap";;
   esac
