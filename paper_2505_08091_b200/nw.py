@@ -322,11 +322,15 @@ def program_source(parts: NwParts) -> Tuple[str, runtime.ProgramInfo, dict]:
         gen_slots = 1
         body += codegen.generate("slot", [r, g], {"s": s}, bounds={"s": (0, LANES - 1)}).source
     tiled = int(parts.nr > 1)
-    # lanes one row apart (skew 1) unless tiles are tall: tiles of >= 2048
-    # rows measured faster with two rows (n = 16384, 4096-row tiles: 1320 vs
-    # 1394 us; 128-row tiles: skew 1 1641 vs 1857 us; strips: skew 1)
+    # lanes one row apart (skew 1) unless tiles are tall, and the boundary
+    # readiness check every 4 steps in tiled programs (every 2 in strips).
+    # Measured at n = 16384 (scripts/ab_nw.py): 4096-row tiles skew 2 / check
+    # every 4: 1212 us (skew 2 / 2: 1320, skew 1 / 4: 1279, skew 1 / 2: 1394);
+    # 128-row tiles skew 1 / 4: 1586 (skew 1 / 2: 1646, skew 2 / 4: 1768);
+    # strips skew 1 / 2: 882 (skew 1 / 4: 897)
     skew = 2 if tiled and parts.h >= 2048 else 1
-    defines = {"NW_TILED": tiled, "NW_GEN_TILES": gen_tiles, "NW_GEN_SLOTS": gen_slots, "NW_SKEW": skew}
+    defines = {"NW_TILED": tiled, "NW_GEN_TILES": gen_tiles, "NW_GEN_SLOTS": gen_slots, "NW_SKEW": skew,
+               "NW_GRP": 4 if tiled else 2}
     head = "".join(f"#ifndef {k}\n#define {k} {v}\n#endif\n" for k, v in defines.items())
     src = (head + _text("lego_index.cuh").replace("#pragma once", "") + "\nnamespace gen {\n" + body + "}\n"
            + _text("nw_kernels.cuh").replace("#pragma once", ""))
