@@ -50,9 +50,10 @@
 //           upper tile's published bottom row the same way;
 //   warp 3  flusher:  converts finished blocks S' -> S and writes them out
 //           as coalesced row segments.
-// Roles synchronise through monotonic block counters in shared memory
-// (loaded / computed / flushed); the compute warp checks them once per 32
-// rows with a prefetched load, so its step body has no barrier.
+// Roles synchronise through monotonic counters in shared memory (loaded /
+// computed / flushed per 32-row block, ready per boundary row); the compute
+// warp checks `loaded` once per block and `ready` every NW_GRP steps against
+// prefetched values, so its step body has no barrier.
 //
 // Includer-provided switches:
 //   NW_TILED      0: one tile per column strip (H = n, no top rows);
