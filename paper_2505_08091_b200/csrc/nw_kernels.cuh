@@ -565,12 +565,20 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
                 if (issued < total_blocks && (issued < NSLOT || ldv_acq(&ctrl->flushed) >= issued - NSLOT)) {
                     const int k = issued;
                     const u32 mb = mbar + 8u * (u32)((gblk + k) % NSLOT);
+#ifndef NW_ABL_NOSIM
                     if (k < tl.nblocks) {
+#else
+                    if (false) {                        // ablation: no sim staging (wrong results)
+#endif
                         const int rows = min(BLK, tl.rows - k * BLK);
                         const u32 blk = ring + (u32)((k % NSLOT) * BLK * ROW_BYTES);
                         if (vec) {
                             const bool ok = tl.col0 + CPL * lane < n;
+#ifndef NW_ABL_SIMCACHED
                             const int* src = simb + (long long)k * BLK * n + tl.col0 + CPL * lane;
+#else
+                            const int* src = simb + tl.col0 + CPL * lane;   // ablation: L2-resident rows (wrong results)
+#endif
 #pragma unroll 8
                             for (int r = 0; r < rows; ++r) {
                                 if (ok) cp_async16(blk + (u32)(r * ROW_BYTES + 16 * slot(k * BLK + r, lane, H)), src);
