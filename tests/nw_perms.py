@@ -176,6 +176,8 @@ def nw_test_layouts(n: int):
     if n <= 128:
         out.append(("strips+rotate", nw_layout(n, cell_order=rotate_cells(max(n, 1)))))
         out.append(("strips+xor", nw_layout(n, tile_rows=128, cell_order=xor_cells(128))))
+    elif n <= 2048:                                  # user cell order where the 256-row ring wraps
+        out.append(("strips+rotate", nw_layout(n, cell_order=rotate_cells(n))))
     if n > 32:
         h = 32 if n <= 128 else 128
         nr, nc = -(-n // h), -(-n // 128)
