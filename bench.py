@@ -731,7 +731,7 @@ def other_kernels(args, pk, world):
                          "GB/s": round((cells * 4 + 16385 ** 2 * 4) / (ms * 1e-3) / 1e9, 1),
                          "layout": NW.describe(lay),
                          "path": ("lego_nw_run (NVRTC program of the layout: " + str(prog.defines) + ")"
-                                  if any(prog.defines.values()) else
+                                  if NW.needs_program(prog.defines) else
                                   "lego_nw_i32 (the layout lowers to no generated map: the library's "
                                   "built-in instance of the template)")}
         del sim, score

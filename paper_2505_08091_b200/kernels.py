@@ -943,7 +943,7 @@ def nw_score(sim, penalty: int, *, layout=None, out=None, stream=None):
         else:
             from . import nw
             prog = nw.nw_program(layout, n, device=sim.device)
-            if not any(prog.defines.values()):
+            if not nw.needs_program(prog.defines):
                 # the layout lowers to no generated map (row-major strips, row-major
                 # ring): the library's nvcc-built instance of the same template
                 runtime.check(runtime.lib().lego_nw_i32(sim.data_ptr(), out.data_ptr(), n, int(penalty), batch,

@@ -303,6 +303,13 @@ def check_cell_order(parts: NwParts, device=None) -> None:
 # program
 # ---------------------------------------------------------------------------
 
+def needs_program(defines: dict) -> bool:
+    """Whether a layout's program differs from the library's built-in strip
+    instance (tiles, a generated tile order or a generated cell order); the
+    tuning defines (NW_SKEW, NW_GRP) do not count."""
+    return any(defines.get(k) for k in ("NW_TILED", "NW_GEN_TILES", "NW_GEN_SLOTS"))
+
+
 def program_source(parts: NwParts) -> Tuple[str, runtime.ProgramInfo, dict]:
     """NVRTC source of the wavefront specialised to the layout's maps."""
     from .kernels import _text

@@ -166,3 +166,11 @@ def test_nw_layout_tiles_batch_and_penalties():
         got = K.nw_score(torch.from_numpy(sim).cuda(), p, layout=lay).cpu().numpy()
         for b in range(3):
             assert np.array_equal(got[b], O.nw(sim[b], p)), (p, b)
+
+
+def test_default_strips_use_the_library_kernel():
+    """Tuning defines (skew, readiness cadence) alone do not require a generated program."""
+    src, info, d = nw.program_source(nw.nw_parts(nw.nw_layout(1000), 1000))
+    assert d["NW_SKEW"] == 1 and not nw.needs_program(d)
+    src, info, d = nw.program_source(nw.nw_parts(nw.nw_layout(4096, tile_rows=2048), 4096))
+    assert d["NW_SKEW"] == 2 and d["NW_GRP"] == 4 and nw.needs_program(d)
