@@ -636,6 +636,61 @@ def run_transpose_shard(args):
     dist.destroy_process_group()
 
 
+def run_nw_band(args):
+    """One NW alignment split by column bands over N GPUs (shard.NwBanded):
+    each rank runs the wavefront over its strips, the band's left edge polled
+    in the previous rank's memory over NVLink inside the kernel -- strong
+    scaling; the check compares this rank's band with the single-GPU kernel.
+    n = 65536 by default (LEGO_NW_BAND_N): at cfg4b's 16384 one GPU already
+    holds all 128 strips at once, so bands cannot shorten the wavefront's
+    critical path; at 65536 one GPU runs 512 strips in ~3.5 waves of 148."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_08091_b200 import kernels as K, shard
+    world, rank, _local = dist_setup(args)
+    if world == 1:                      # symmetric memory needs a process group, even of one rank
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0,
+                                device_id=torch.device("cuda", 0))
+    n = int(os.environ.get("LEGO_NW_BAND_N", "65536"))
+    g = torch.Generator(device="cuda").manual_seed(4)
+    sim = torch.randint(-10, 11, (n, n), generator=g, device="cuda", dtype=torch.int32)
+    nb = shard.NwBanded(n, 1, sim.device)
+    score = torch.empty(n + 1, n + 1, dtype=torch.int32, device="cuda")
+    step = lambda: nb(sim, 10, out=score)  # noqa: E731
+    step()
+    torch.cuda.synchronize()
+    whole = K.nw_score(sim, 10)
+    lo, hi = 1 + 128 * nb.begin, min(n, 128 * nb.end) + 1
+    ok = torch.equal(score[:, lo:hi], whole[:, lo:hi]) and torch.equal(score[0], whole[0])
+    del whole
+    launches0 = K.LAUNCHES[0]
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        ms = time_steps(step, args.steps, args.warmup, world)
+    launches = K.LAUNCHES[0] - launches0 - 2 * args.warmup
+    ms_step = ms / args.steps
+    cells = n * n
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(cells / (ms_step * 1e-3) / 1e9, 1), "unit": "GCUPS",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+                "data": "synthetic (uniform sim in [-10, 10], penalty 10)",
+                "config": {"workload": f"cfg4b kernel on one {n}x{n} NW alignment in column bands over N GPUs "
+                                       "(shard.NwBanded: the band's left edge polled in the peer's memory "
+                                       "over NVLink inside the wavefront kernel)", "n": n,
+                           "bands": nb.bands, "check_own_band": "ok" if ok else "MISMATCH",
+                           "parallelism": f"strong: {world} column bands, edge hand-off inside the kernel"},
+                "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
+                "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def lower_size(layout):
     from paper_2505_08091_b200 import lower
     return lower.physical_size(layout)
@@ -760,10 +815,11 @@ def main():
     ap.add_argument("--impl", default="lego", choices=["lego", "reference"])
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="remap", choices=["remap", "gemm_b8", "transpose_shard"],
+    ap.add_argument("--workload", default="remap", choices=["remap", "gemm_b8", "transpose_shard", "nw_band"],
                     help="remap: headline cfg2 (weak scaling, one matrix per GPU); gemm_b8: cfg5 batch of 8 "
                          "8192^3 GEMMs split 8/N per GPU (strong); transpose_shard: one 16384^2 bf16 matrix "
-                         "row-sharded over N GPUs into the Col layout by the fused routed transpose (strong)")
+                         "row-sharded over N GPUs into the Col layout by the fused routed transpose (strong); "
+                         "nw_band: one 16384^2 NW alignment in column bands over N GPUs (strong)")
     ap.add_argument("--dry-run", action="store_true", help="launch and rendezvous only (CPU, gloo)")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -778,6 +834,8 @@ def main():
         run_gemm_b8(args)
     elif args.workload == "transpose_shard":
         run_transpose_shard(args)
+    elif args.workload == "nw_band":
+        run_nw_band(args)
     else:
         run(args)
 

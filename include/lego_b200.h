@@ -193,6 +193,23 @@ lego_status lego_softmax_offsets(lego_program p, int64_t *out, int64_t rows, voi
 lego_status lego_nw_i32(const int32_t *sim, int32_t *score, int64_t n, int32_t penalty,
                         int64_t batch, void *stream);
 
+/* Column band of the strip-mode recurrence: strips [strip_begin, strip_end)
+ * (128 columns each) of every matrix, written into the full-size score; the
+ * multi-GPU single-alignment path (one band per GPU, paper_2505_08091_b200
+ * shard.nw_score_banded).  bnd_words: this band's right-edge columns, batch x
+ * (strip_end - strip_begin) x n_pad int32 (n_pad = n rounded up to 32),
+ * 16-byte aligned, preset by the caller to bytes 0x80 before any band that
+ * reads it starts; left_words: the previous band's last edge column (matrix b
+ * at left_words + b * left_batch_stride; a peer GPU's memory over NVLink), or
+ * NULL when strip_begin == 0.  Edges are stored and polled at system scope.
+ * max_ctas > 0 caps the persistent grid (bands sharing one GPU must all be
+ * resident).  Other rules as lego_nw_i32.  Replaces no reference interface
+ * (the reference has no NW kernel; SURVEY.md 8(e) "next" row). */
+lego_status lego_nw_band_i32(const int32_t *sim, int32_t *score, int64_t n, int32_t penalty,
+                             int64_t batch, int64_t strip_begin, int64_t strip_end, int32_t *bnd_words,
+                             const int32_t *left_words, int64_t left_batch_stride, int32_t max_ctas,
+                             void *stream);
+
 /* The same recurrence through a program generated from a LEGO layout of the
  * cell grid (kernels.nw_layout / nw_program, LEGO_PROG_NW):
  *   GroupBy([NR*H, NC*128]).OrderBy(RegP([NR,H,NC,128],[1,3,2,4])).OrderBy(T, I)

@@ -184,6 +184,12 @@ __device__ __forceinline__ int ld_bnd(const int* p) {
     asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(w) : "l"(p) : "memory");
     return w;
 }
+// system scope: a column band's edge polled by the next GPU over NVLink
+__device__ __forceinline__ int ld_bnd_sys(const int* p) {
+    int w;
+    asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(w) : "l"(p) : "memory");
+    return w;
+}
 __device__ __forceinline__ int4 ld_bnd4(const int* p) {
     int4 w;
     asm volatile("ld.relaxed.gpu.global.v4.b32 {%0,%1,%2,%3}, [%4];"
@@ -264,8 +270,19 @@ __device__ __forceinline__ void ldsv<4>(u32 a, int (&v)[4]) {
                  : "r"(a));
 }
 
-// predicated (branch-free) publication of RPS consecutive boundary words
+// predicated (branch-free) publication of RPS consecutive boundary words;
+// SYS: system scope (column bands: the next GPU polls them)
+template <bool SYS>
 __device__ __forceinline__ void publish(int* p, int pred, const int (&v)[RPS]) {
+#if NW_RPS == 4
+    if (SYS) {
+        asm volatile(
+            "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\t"
+            "@q st.relaxed.sys.global.v4.b32 [%0], {%2, %3, %4, %5};\n\t}"
+            :: "l"(p), "r"(pred), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]) : "memory");
+        return;
+    }
+#endif
 #if NW_RPS == 8
     asm volatile(
         "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\t"
@@ -320,7 +337,7 @@ struct Tile {
 // r0 = RPS*s - SKEW*(j+1) .. r0+RPS-1, columns 4j..4j+3 of the tile.  Row q's
 // left value is lane j-1's last column of its slot q-SKEW: from this step when
 // q >= SKEW, else from the previous one.
-template <bool GUARD>
+template <bool GUARD, bool BAND>
 __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char* ring, u32 bnd, int p2, const Tile& tl,
                                         int h, int* pub_row) {
     const int r0 = RPS * s - SKEW * (lane + 1);
@@ -416,7 +433,7 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char*
     // multiple of 4, so its RPS rows are all live or all not)
     const int pub = (lane == 31) & (r0 >= 0) & (r0 < tl.rows);
 #ifndef NW_ABL_NOPUB
-    publish(pub_row, pub, c.send);
+    publish<BAND>(pub_row, pub, c.send);
 #endif
 #ifdef LEGO_NW_DEBUG
     if (pub && r0 < 512) NW_TRACE(3, 1536 + r0 / 4);   // lane 31 published rows r0..r0+3
@@ -425,7 +442,7 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char*
 
 // one block of STEPS steps (lane 0's rows 32k - SKEW ..); boundary readiness is
 // checked every GRP steps against a counter value prefetched GRP steps earlier
-template <bool GUARD>
+template <bool GUARD, bool BAND>
 __device__ __forceinline__ void nw_block(Lane& c, int k, int lane, unsigned char* ring, u32 bnd, int p2, const Tile& tl,
                                          int h, int& rd, const int* ready, int rows_total) {
     int* pub_blk = tl.my_bnd + tl.row0 + k * BLK - 32 * SKEW;  // lane 31's rows of step u: + RPS*u
@@ -438,7 +455,7 @@ __device__ __forceinline__ void nw_block(Lane& c, int k, int lane, unsigned char
             rd = ldv(ready);
             if (lane == 0 && s < 512) NW_TRACE(0, 1536 + s);   // readiness check passed
         }
-        nw_step<GUARD>(c, s, lane, ring, bnd, p2, tl, h, pub_blk + RPS * u);
+        nw_step<GUARD, BAND>(c, s, lane, ring, bnd, p2, tl, h, pub_blk + RPS * u);
     }
 }
 
@@ -447,9 +464,17 @@ __device__ __forceinline__ void nw_block(Lane& c, int k, int lane, unsigned char
 // bnd_g: per (matrix, tile column) n_pad words (the column's right edge,
 // by interior row); top_g (tiled): per (matrix, tile) 128 words (the bottom
 // row of the tile above it).  Both preset to NW_EMPTY by the launcher.
+// BAND (strip mode): this launch owns strips strip_base .. strip_base +
+// nc_band - 1 of the matrices' nc; bnd_g holds only those strips' edge
+// columns, and the first one's left edge is read from left_ext (the previous
+// band's last edge column, possibly another GPU's memory; matrix bm at
+// left_ext + bm * left_bstride)
+template <bool BAND = false>
 __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* __restrict__ score, int n, int p,
                                               int H, int nr, int nc, int total, int* __restrict__ ticket,
-                                              int* __restrict__ bnd_g, int* __restrict__ top_g) {
+                                              int* __restrict__ bnd_g, int* __restrict__ top_g,
+                                              int strip_base = 0, int nc_band = 0, const int* left_ext = nullptr,
+                                              long long left_bstride = 0) {
     extern __shared__ __align__(16) unsigned char smem[];
     int* ring_gen = reinterpret_cast<int*>(smem);
     Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem + RING_BYTES + BND_BYTES + MBAR_BYTES);
@@ -463,7 +488,8 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
     const int lane = threadIdx.x & 31;
     const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);   // warp-uniform role
     const int n_pad = (n + BLK - 1) / BLK * BLK;
-    const int tiles_per_matrix = nr * nc;
+    const int ncb = BAND ? nc_band : nc;             // tile columns this launch owns
+    const int tiles_per_matrix = nr * ncb;
 
     for (;;) {
         if (threadIdx.x == 0) {
@@ -480,12 +506,13 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
 #endif
         Tile tl;
         tl.bm = t / tiles_per_matrix;
-        tile_of(t - tl.bm * tiles_per_matrix, nc, tl.a, tl.b);
+        tile_of(t - tl.bm * tiles_per_matrix, ncb, tl.a, tl.b);
+        if (BAND) tl.b += strip_base;
         tl.row0 = tl.a * H;
         tl.col0 = tl.b * STRIP;
         tl.rows = min(H, n - tl.row0);
         tl.nblocks = (tl.rows + BLK - 1) / BLK;
-        tl.my_bnd = bnd_g + (long long)(tl.bm * nc + tl.b) * n_pad;
+        tl.my_bnd = bnd_g + (long long)(tl.bm * ncb + (tl.b - (BAND ? strip_base : 0))) * n_pad;
 #if NW_TILED
         {
             const long long tid = (long long)tl.bm * tiles_per_matrix + (long long)tl.a * nc + tl.b;
@@ -541,9 +568,9 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
                 }
                 pl = ldv(&ctrl->loaded);                // prefetch for the next block
                 if (k < LAG_BLKS || (NW_TILED && k + 1 >= tl.nblocks))   // lane 31's first rows are negative; tiled: rows past the tile
-                    nw_block<true>(c, k, lane, smem, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
+                    nw_block<true, BAND>(c, k, lane, smem, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
                 else
-                    nw_block<false>(c, k, lane, smem, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
+                    nw_block<false, BAND>(c, k, lane, smem, bnd, p2, tl, H, rd, &ctrl->ready, rows_total);
             }
 #if NW_TILED
             // the tile's last row (each lane's state stopped there) goes to the tile below
@@ -662,7 +689,8 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
             // prefix of the group is in.  Row r sits at ring index r + SKEW,
             // so lane 0's rows 4s - SKEW .. 4s - SKEW + 3 are one aligned
             // 16-byte load.
-            const int* left = tl.my_bnd - n_pad + tl.row0;
+            const bool ext = BAND && tl.b == strip_base && left_ext != nullptr;   // the previous band's edge
+            const int* left = ext ? left_ext + tl.bm * left_bstride + tl.row0 : tl.my_bnd - n_pad + tl.row0;
             const int groups = tl.nblocks + DRAIN;
             for (int m = 0; m < groups; ++m) {
                 const int r = m * BLK + lane;
@@ -672,7 +700,7 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
                 int v = 0;                              // S'[r+1][0] = 0 on the matrix edge
                 bool ok = true;
                 if (tl.b > 0 && r < tl.rows) {
-                    v = ld_bnd(left + r);
+                    v = ext ? ld_bnd_sys(left + r) : ld_bnd(left + r);
                     ok = v != NW_EMPTY;
                 }
                 bool written = false;
@@ -697,7 +725,7 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
                     if (tt == 32) break;
                     if (NW_POLL_NS) __nanosleep(NW_POLL_NS);
                     if (!ok) {
-                        v = ld_bnd(left + r);
+                        v = ext ? ld_bnd_sys(left + r) : ld_bnd(left + r);
                         ok = v != NW_EMPTY;
                     }
                 }
@@ -791,6 +819,17 @@ lego_nw_tiles(const int* __restrict__ sim, int* __restrict__ score, int n, int p
               int* __restrict__ ticket, int* __restrict__ bnd_g, int* __restrict__ top_g) {
     nwk::nw_tiles_body(sim, score, n, p, H, nr, nc, total, ticket, bnd_g, top_g);
 }
+
+#ifdef NW_BAND_ENTRY
+// column band of strip-mode tiles (multi-GPU single alignment, shard.py)
+NW_GLOBAL void __launch_bounds__(128, 1)
+lego_nw_band(const int* __restrict__ sim, int* __restrict__ score, int n, int p, int nc, int total,
+             int* __restrict__ ticket, int* __restrict__ bnd_g, int strip_base, int nc_band,
+             const int* __restrict__ left_ext, long long left_bstride) {
+    nwk::nw_tiles_body<true>(sim, score, n, p, n, 1, nc, total, ticket, bnd_g, nullptr, strip_base, nc_band,
+                             left_ext, left_bstride);
+}
+#endif
 
 NW_GLOBAL void lego_nw_borders(int* __restrict__ score, long long n, int p, long long batch) {
     nwk::nw_borders_body(score, n, p, batch);

@@ -18,6 +18,7 @@
 #include "lego_common.h"
 
 #define NW_GLOBAL static __global__
+#define NW_BAND_ENTRY 1
 #include "nw_kernels.cuh"
 
 #ifdef LEGO_NW_DEBUG
@@ -127,4 +128,51 @@ extern "C" lego_status lego_nw_i32(const int32_t* sim, int32_t* score, int64_t n
     lego_nw_tiles<<<pl.ctas, 128, pl.smem, st>>>(sim, score, (int)n, penalty, pl.H, pl.nr, pl.nc, pl.total,
                                                   pl.ticket, pl.bnd, pl.top);
     return lego_cuda_check(cudaGetLastError(), "nw launch");
+}
+
+// Column band of a strip-mode NW (multi-GPU single alignment: shard.nw_score_banded).
+// This launch computes strips [strip_begin, strip_end) of every matrix into the
+// full-size score; bnd_words holds those strips' right-edge columns (batch x
+// strips x n_pad int32, n_pad = n rounded up to 32), preset by the caller to
+// the 0x80808080 sentinel before any reader starts; left_words is the previous
+// band's last edge column (matrix b at left_words + b * left_batch_stride),
+// possibly a peer GPU's memory, or null when strip_begin == 0.  Edges are
+// published and polled at system scope.  max_ctas > 0 caps the persistent
+// grid (several bands sharing one GPU must all be resident).
+extern "C" lego_status lego_nw_band_i32(const int32_t* sim, int32_t* score, int64_t n, int32_t penalty,
+                                        int64_t batch, int64_t strip_begin, int64_t strip_end, int32_t* bnd_words,
+                                        const int32_t* left_words, int64_t left_batch_stride, int32_t max_ctas,
+                                        void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n < 1 || batch < 0) return lego_fail(LEGO_E_SHAPE, "NW band needs n >= 1");
+    const long long nc = (n + nwk::STRIP - 1) / nwk::STRIP;
+    if (strip_begin < 0 || strip_end > nc || strip_begin >= strip_end)
+        return lego_fail(LEGO_E_SHAPE, "strip band [%lld, %lld) outside [0, %lld)", (long long)strip_begin,
+                         (long long)strip_end, nc);
+    if (!bnd_words || ((uintptr_t)bnd_words & 15)) return lego_fail(LEGO_E_ARG, "bnd_words must be 16-byte aligned");
+    if ((strip_begin > 0) != (left_words != nullptr))
+        return lego_fail(LEGO_E_ARG, "left_words is required exactly when the band does not start at strip 0");
+    const long long n_pad = (n + nwk::BLK - 1) / nwk::BLK * nwk::BLK;
+    if (left_words && left_batch_stride < n_pad) return lego_fail(LEGO_E_ARG, "left_batch_stride below n_pad");
+    NwPlan pl;
+    LEGO_TRY(lego_nw_prepare(sim, score, n, penalty, batch, n, 0, st, &pl));   // validation, borders grid
+    if (batch == 0) return LEGO_OK;
+    int* ticket = nullptr;
+    int* unused = nullptr;
+    LEGO_TRY(nw_scratch(st, 0, &ticket, &unused));
+    const long long nb = strip_end - strip_begin;
+    const long long total = nb * batch;
+    if (total > INT32_MAX / 2) return lego_fail(LEGO_E_SHAPE, "NW band batch too large");
+    int dev = 0, sms = 148;
+    LEGO_TRY(lego_cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    long long ctas = total < sms ? total : sms;
+    if (max_ctas > 0 && ctas > max_ctas) ctas = max_ctas;
+    lego_nw_borders<<<pl.border_ctas, 256, 0, st>>>(score, n, penalty, batch);
+    static std::atomic<unsigned long long> attr_set{0};
+    LEGO_TRY(lego_smem_optin(lego_nw_band, nwk::SMEM_BYTES, attr_set, "cudaFuncSetAttribute(nw band)"));
+    lego_nw_band<<<(unsigned)ctas, 128, nwk::SMEM_BYTES, st>>>(sim, score, (int)n, penalty, (int)nc, (int)total,
+                                                               ticket, bnd_words, (int)strip_begin, (int)nb,
+                                                               left_words, (long long)left_batch_stride);
+    return lego_cuda_check(cudaGetLastError(), "nw band launch");
 }

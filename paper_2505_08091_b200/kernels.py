@@ -955,6 +955,57 @@ def nw_score(sim, penalty: int, *, layout=None, out=None, stream=None):
     return out
 
 
+NW_EMPTY_WORD = -2139062144        # 0x80808080: the sentinel of not-yet-published NW edge words
+
+
+def nw_band_words(n: int, strips: int, batch: int = 1) -> int:
+    """int32 words of a band's edge columns (``bnd`` of :func:`nw_score_band`)."""
+    return batch * strips * (-(-n // 32) * 32)
+
+
+def nw_score_band(sim, penalty: int, strips, bnd, *, left=None, left_strips: int = 0, out=None,
+                  max_ctas: int = 0, stream=None):
+    """Strips ``strips = (begin, end)`` (128 columns each) of the NW score of
+    ``sim`` into ``out`` (full (..., n+1, n+1) size; only those columns and the
+    borders are written).  ``bnd`` (int32, :func:`nw_band_words` words, preset
+    to :data:`NW_EMPTY_WORD` before any reader starts) receives the band's edge
+    columns (batch x strips x n_pad, n_pad = n rounded up to 32); ``left`` is
+    the previous band's ``bnd`` tensor with ``left_strips`` strips, possibly a
+    peer GPU's symmetric-memory buffer: its last strip's column is read
+    (``None`` when ``begin == 0``).  The multi-GPU building block of
+    :func:`.shard.nw_score_banded`."""
+    torch = _torch()
+    if sim.dtype != torch.int32 or not sim.is_cuda or sim.dim() < 2 or sim.shape[-1] != sim.shape[-2]:
+        raise ShapeMismatch("nw_score_band takes a CUDA int32 tensor of shape (..., n, n)")
+    sim = sim.contiguous()
+    n = sim.shape[-1]
+    batch = 1
+    for d in sim.shape[:-2]:
+        batch *= d
+    begin, end = (int(x) for x in strips)
+    shape = (*sim.shape[:-2], n + 1, n + 1)
+    if out is None:
+        out = torch.empty(*shape, dtype=torch.int32, device=sim.device)
+    else:
+        _check_out(out, shape, torch.int32, sim.device, "nw_score_band")
+    if bnd.dtype != torch.int32 or bnd.device != sim.device or bnd.numel() < nw_band_words(n, end - begin, batch):
+        raise ShapeMismatch("bnd must be int32 on sim's device with nw_band_words(n, strips, batch) words")
+    left_ptr, left_stride = None, 0
+    if left is not None:
+        n_pad = -(-n // 32) * 32
+        if left_strips < 1 or left.numel() < nw_band_words(n, left_strips, batch):
+            raise ShapeMismatch("left must hold the previous band's left_strips edge columns per matrix")
+        left_ptr = left.data_ptr() + 4 * (left_strips - 1) * n_pad     # its last strip
+        left_stride = left_strips * n_pad
+    with torch.cuda.device(sim.device):
+        st = runtime.stream_handle(stream)
+        runtime.check(runtime.lib().lego_nw_band_i32(sim.data_ptr(), out.data_ptr(), n, int(penalty), batch, begin,
+                                                     end, bnd.data_ptr(), left_ptr, int(left_stride),
+                                                     int(max_ctas), st), "lego_nw_band_i32")
+    LAUNCHES[0] += 2
+    return out
+
+
 # measured (scripts/ab_gemm_group.py, 8192^3, 4 alternating runs each): G = 32 685 us,
 # 24 688, 48 688, 16 692, 64 695
 GEMM_RASTER_GROUP = int(os.environ.get("LEGO_GEMM_GROUP", "32"))

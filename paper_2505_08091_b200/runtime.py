@@ -85,6 +85,7 @@ SIGS = {
     "lego_softmax_f32": ([VP, VP, I64, I64, VP], I32),
     "lego_nw_i32": ([VP, VP, I64, I32, I64, VP], I32),
     "lego_nw_run": ([VP, VP, VP, I64, I32, I64, VP], I32),
+    "lego_nw_band_i32": ([VP, VP, I64, I32, I64, I64, I64, VP, VP, I64, I32, VP], I32),
     "lego_softmax_run": ([VP, VP, VP, I64, I64, VP], I32),
     "lego_softmax_offsets": ([VP, VP, I64, VP], I32),
     "lego_gemm_raster": ([VP, I64, I64, I64, I32, VP], I32),

@@ -13,7 +13,10 @@ has to cross shards:
   column-block tiles, then each rank finishes with local LEGO remaps;
 * :func:`transpose_rows_fused` -- the same result as one routed transpose
   kernel per rank that stores straight into the other ranks' shards through
-  NVLink peer memory (torch symmetric memory), no NCCL in the data path.
+  NVLink peer memory (torch symmetric memory), no NCCL in the data path;
+* :class:`NwBanded` -- one Needleman-Wunsch alignment split by column bands,
+  the wavefront kernel of each band polling the previous band's edge column
+  in the peer GPU's memory (the hand-off inside the kernel).
 
 All functions take ``compute=`` so the host logic is testable on CPU with
 the ``gloo`` backend (tests/test_shard.py injects the oracle); the default
@@ -105,6 +108,103 @@ def gather_shards(local, p: ShardPlan, group=None):
         dist.all_gather(parts, local.contiguous(), group=group)
         full = torch.cat(parts)
     return full[:p.total]
+
+
+def nw_bands(n: int, world: int):
+    """Strip ranges [begin, end) (128-column strips) of an n x n NW per rank:
+    contiguous, as even as whole strips allow (ranks past the last strip get
+    an empty band)."""
+    nc = -(-n // 128)
+    per = -(-nc // world) if world else 0
+    return [(min(nc, r * per), min(nc, (r + 1) * per)) for r in range(world)]
+
+
+class NwBanded:
+    """One Needleman-Wunsch alignment (or a batch) split by column bands over
+    the ranks, set up once (symmetric edge buffer, peer view) and run per call.
+
+    Rank r computes strips ``nw_bands(n, world)[r]`` of every matrix with the
+    wavefront kernel, reading the previous band's edge column straight from
+    rank r-1's memory over NVLink (torch symmetric memory, system-scope
+    sentinel words): the hand-off is inside the kernel, no NCCL on the data
+    path; the band's own right edge lands in its symmetric buffer for rank
+    r+1.  Each call presets the edge words, device-barriers, runs the band and
+    device-barriers again (the next band has read the edge), all on the
+    current stream.  SURVEY.md 8(e): the NW row's "next" item."""
+
+    def __init__(self, n: int, batch: int, device, *, group=None, max_ctas: int = 0):
+        import torch
+        from torch.distributed import _symmetric_memory as symm
+        from . import kernels
+        dist = _dist()
+        self.world, self.rank = world_and_rank(group)
+        self.n, self.batch, self.group, self.max_ctas = n, batch, group, max_ctas
+        self.bands = nw_bands(n, self.world)
+        self.begin, self.end = self.bands[self.rank]
+        strips_max = max(e - b for b, e in self.bands)
+        self.bnd = symm.empty(max(1, kernels.nw_band_words(n, strips_max, batch)), dtype=torch.int32, device=device)
+        self.handle = symm.rendezvous(self.bnd, group if group is not None else dist.group.WORLD)
+        self.left, self.left_strips = None, 0
+        if self.begin > 0:
+            pb, pe = self.bands[self.rank - 1]
+            self.left = self.handle.get_buffer(self.rank - 1, (self.bnd.numel(),), torch.int32)
+            self.left_strips = pe - pb
+
+    def __call__(self, sim, penalty: int, *, out=None, gather: bool = False):
+        import torch
+        from . import kernels
+        n = self.n
+        if sim.shape[-1] != n or sim.numel() != self.batch * n * n:
+            raise ShapeMismatch(f"sim {tuple(sim.shape)} does not match the banded plan ({self.batch} x {n} x {n})")
+        if out is None:
+            out = torch.empty(*sim.shape[:-2], n + 1, n + 1, dtype=torch.int32, device=sim.device)
+        self.bnd.fill_(kernels.NW_EMPTY_WORD)
+        self.handle.barrier(channel=0)          # every band's edge words are preset before any band runs
+        if self.end > self.begin:
+            kernels.nw_score_band(sim, penalty, (self.begin, self.end), self.bnd, left=self.left,
+                                  left_strips=self.left_strips, out=out, max_ctas=self.max_ctas)
+        else:                                   # no strip for this rank: borders only
+            edge = -torch.arange(n + 1, device=sim.device, dtype=torch.int32) * int(penalty)
+            out[..., 0, :] = edge
+            out[..., :, 0] = edge
+        self.handle.barrier(channel=0)          # the next band has read this band's edge
+        if not gather or self.world == 1:
+            return out
+        return gather_nw_bands(out, self.bands, group=self.group)
+
+
+def nw_score_banded(sim, penalty: int, *, group=None, gather: bool = True, max_ctas: int = 0):
+    """:class:`NwBanded` for one call: every rank passes the (replicated)
+    ``sim``; with ``gather=True`` every rank returns the full score (bands
+    all-gathered), else the full-size score with only this rank's columns
+    (and the borders) written."""
+    batch = 1
+    for d in sim.shape[:-2]:
+        batch *= d
+    return NwBanded(sim.shape[-1], batch, sim.device, group=group, max_ctas=max_ctas)(sim, penalty, gather=gather)
+
+
+def gather_nw_bands(out, bands, *, group=None):
+    """All-gather the column bands of full-size NW scores (each rank's
+    ``out`` holds its band's columns 1 + 128*begin .. 128*end, plus the borders)."""
+    import torch
+    dist = _dist()
+    n = out.shape[-1] - 1
+    w = 128 * max(e - b for b, e in bands)
+    lead = out.shape[:-2]
+    rank = world_and_rank(group)[1]
+    b0, e0 = bands[rank]
+    c0, c1 = 1 + 128 * b0, min(n, 128 * e0) + 1
+    mine = out.new_zeros(*lead, n + 1, w)
+    mine[..., :, :c1 - c0] = out[..., :, c0:c1]
+    parts = [torch.empty_like(mine) for _ in bands]
+    dist.all_gather(parts, mine.contiguous(), group=group)
+    full = out.clone()
+    for (b, e), part in zip(bands, parts):
+        lo, hi = 1 + 128 * b, min(n, 128 * e) + 1
+        if hi > lo:
+            full[..., :, lo:hi] = part[..., :, :hi - lo]
+    return full
 
 
 def transpose_rows(local_rows, n_rows: int, n_cols: int, *, group=None,

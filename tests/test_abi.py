@@ -55,6 +55,15 @@ def test_null_arguments_fail_cleanly():
     st = lib.lego_nw_i32(aligned + 4, aligned, 16, 10, 1, None)
     assert st == 8 and b"16-byte aligned" in lib.lego_last_error()
     assert lib.lego_nw_i32(aligned, aligned, 16, 10, 0, None) == 0     # empty batch
+    # NW column band (multi-GPU single alignment): band and edge arguments
+    st = lib.lego_nw_band_i32(aligned, aligned, 300, 10, 1, 2, 4, aligned, None, 0, 0, None)
+    assert st == 3 and b"strip band" in lib.lego_last_error()         # 300 columns = 3 strips
+    st = lib.lego_nw_band_i32(aligned, aligned, 300, 10, 1, 1, 3, aligned, None, 0, 0, None)
+    assert st == 8 and b"left_words" in lib.lego_last_error()         # band after strip 0 needs the left edge
+    st = lib.lego_nw_band_i32(aligned, aligned, 300, 10, 1, 0, 3, aligned + 4, None, 0, 0, None)
+    assert st == 8 and b"16-byte aligned" in lib.lego_last_error()
+    st = lib.lego_nw_band_i32(aligned, aligned, 300, 10, 1, 1, 3, aligned, aligned, 8, 0, None)
+    assert st == 8 and b"left_batch_stride" in lib.lego_last_error()
 
 
 @pytest.mark.parametrize("dsl", [

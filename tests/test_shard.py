@@ -156,3 +156,13 @@ def test_fused_transpose_plan_proves_vector_routing():
     bad = kernels.Route(2, lambda v: (v % 2, v // 2), ("bad",))
     with pytest.raises(L.UnsupportedNode):
         kernels.plan_remap(None, layout, 4, bad)
+
+
+def test_nw_bands_cover_the_strips_in_order():
+    from paper_2505_08091_b200 import shard
+    for n, world in ((16384, 8), (16384, 3), (300, 4), (100, 2), (1, 1), (129, 2)):
+        bands = shard.nw_bands(n, world)
+        nc = -(-n // 128)
+        assert len(bands) == world and bands[0][0] == 0 and bands[-1][1] == nc
+        assert all(b0[1] == b1[0] for b0, b1 in zip(bands, bands[1:]))
+        assert all(e >= b for b, e in bands)
