@@ -7,7 +7,20 @@ import torch  # noqa: E402
 
 import paper_2505_08091_b200 as L  # noqa: E402
 from paper_2505_08091_b200 import kernels as K  # noqa: E402
-from scripts.quick_time import t  # noqa: E402
+
+
+def t(fn, iters=30, warm=5):
+    """Median-free mean time (ms) of fn over `iters` launches after `warm`, CUDA events."""
+    for _ in range(warm):
+        fn()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
 
 g = L.parse_layout("GroupBy([16384,16384]).OrderBy(Col(16384,16384))")
 for dt in (torch.bfloat16, torch.float32):
