@@ -750,15 +750,36 @@ __device__ __forceinline__ void nw_tiles_body(const int* __restrict__ sim, int* 
                 int off = (tl.row0 + k * BLK + tl.col0 + lane + 2) * p;   // (i + j) * p of column lane, row k*BLK
 #if NW_GEN_SLOTS
                 // cell (r, 32q + lane) sits at slot(r, (32q + lane) / 4) * 4 + lane % 4 of its ring row
-#pragma unroll 2
-                for (int r = 0; r < rows; ++r) {
+                if (rows == BLK && tl.col0 + STRIP <= n) {
+                    // full block: 16 rows of loads in flight before their stores
 #pragma unroll
-                    for (int q = 0; q < CPL; ++q)
-                        if (ok[q])
-                            dst[32 * q] = src[r * STRIP + 4 * slot(k * BLK + r, 8 * q + (lane >> 2), H) + (lane & 3)]
-                                          - (off + 32 * q * p);
-                    dst += ld;
-                    off += p;
+                    for (int hh = 0; hh < 2; ++hh) {
+                        int v[16][CPL];
+#pragma unroll
+                        for (int r = 0; r < 16; ++r)
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q)
+                                v[r][q] = src[(16 * hh + r) * STRIP
+                                              + 4 * slot(k * BLK + 16 * hh + r, 8 * q + (lane >> 2), H) + (lane & 3)];
+#pragma unroll
+                        for (int r = 0; r < 16; ++r) {
+                            int* d = dst + (16 * hh + r) * ld;
+                            const int o = off + (16 * hh + r) * p;
+#pragma unroll
+                            for (int q = 0; q < CPL; ++q) d[32 * q] = v[r][q] - (o + 32 * q * p);
+                        }
+                    }
+                } else {
+#pragma unroll 2
+                    for (int r = 0; r < rows; ++r) {
+#pragma unroll
+                        for (int q = 0; q < CPL; ++q)
+                            if (ok[q])
+                                dst[32 * q] = src[r * STRIP + 4 * slot(k * BLK + r, 8 * q + (lane >> 2), H) + (lane & 3)]
+                                              - (off + 32 * q * p);
+                        dst += ld;
+                        off += p;
+                    }
                 }
 #else
                 if (rows == BLK && tl.col0 + STRIP <= n) {

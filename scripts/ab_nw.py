@@ -18,6 +18,10 @@ if _which == "tiles4096":
     _lay = nw.nw_layout(n, tile_rows=4096, tile_order=skew_order(4, 128))
 elif _which == "tiles128":
     _lay = nw.nw_layout(n, tile_rows=128, tile_order="antidiag")
+elif _which in ("strips_rotate", "strips_xor"):   # strips with a user GenP cell order (NW_GEN_SLOTS)
+    sys.path.insert(0, "tests")
+    from nw_perms import rotate_cells, xor_cells
+    _lay = nw.nw_layout(n, cell_order=(rotate_cells if _which == "strips_rotate" else xor_cells)(n))
 else:
     _lay = nw.nw_layout(n)
 parts = nw.nw_parts(_lay, n)
