@@ -14,6 +14,8 @@ has to cross shards:
 * :func:`transpose_rows_fused` -- the same result as one routed transpose
   kernel per rank that stores straight into the other ranks' shards through
   NVLink peer memory (torch symmetric memory), no NCCL in the data path;
+* :func:`remap_sharded` -- any bijective layout over one array split across
+  ranks (destination positions by the GPU map, one uneven all-to-all);
 * :class:`NwBanded` -- one Needleman-Wunsch alignment split by column bands,
   the wavefront kernel of each band polling the previous band's edge column
   in the peer GPU's memory (the hand-off inside the kernel).
@@ -244,6 +246,67 @@ def transpose_rows(local_rows, n_rows: int, n_cols: int, *, group=None,
     tt = run(recv, None, t_layout)                          # (world, C*R), each C x R
     # place tiles side by side: out[c, q*R + r] = tt[q, c*R + r]
     return run(tt.reshape(-1), None, _sidebyside_layout(R, C, world)).reshape(C, world * R)
+
+
+def remap_sharded(local, layout, *, group=None, compute_map: Optional[Callable] = None):
+    """Any bijective layout applied to ONE array split over the ranks.
+
+    Rank r holds the logical elements [r*Lp, (r+1)*Lp) (row-major logical
+    index, Lp = ceil(N / world)); it returns its share [r*Pp, (r+1)*Pp) of the
+    physical result ``y[layout.apply(v)] = x[v]`` (Pp = ceil(N / world)).
+
+    Step 1 (local, LEGO): the destination positions of the local range --
+    ``kernels.apply_map(layout, first=, count=)`` on the GPU.  Step 2: bucket
+    the elements by owning rank and exchange values and in-shard offsets with
+    two ``all_to_all_single`` calls (uneven splits).  Step 3 (local): place the
+    received values.  The generic path of SURVEY.md 8(e) for single-matrix
+    layouts that are not digit permutations (e.g. cfg4a's anti-diagonal
+    GenP); ``compute_map(layout, first, count)`` replaces the GPU map in CPU
+    tests."""
+    import torch
+    from . import lower
+    dist = _dist()
+    world, rank = world_and_rank(group)
+    n = lower.logical_size(layout)
+    if lower.physical_size(layout) != n or getattr(layout, "injective", False):
+        raise ShapeMismatch("remap_sharded needs a bijective layout (logical size == physical size)")
+    lp = -(-n // world)
+    start = min(n, rank * lp)
+    count = min(n, start + lp) - start
+    flat = local.reshape(-1)
+    if flat.numel() != count:
+        raise ShapeMismatch(f"rank {rank} holds {flat.numel()} elements, expected {count} of {n}")
+    if compute_map is None:
+        from . import kernels
+        pos = kernels.apply_map(layout, dtype=torch.int64, device=flat.device, first=start, count=count)
+    else:
+        pos = compute_map(layout, start, count).to(flat.device)
+    pos = pos.to(torch.int64)
+    owner = torch.div(pos, lp, rounding_mode="floor")
+    order = torch.argsort(owner, stable=True)
+    vals = flat[order].contiguous()
+    offs = (pos - owner * lp)[order].contiguous()
+    send = torch.bincount(owner, minlength=world).to(torch.int64)
+    recv = torch.empty_like(send)
+    if world > 1:
+        dist.all_to_all_single(recv, send, group=group)
+    else:
+        recv.copy_(send)
+    sc, rc = [int(v) for v in send.tolist()], [int(v) for v in recv.tolist()]
+    rvals = flat.new_empty(sum(rc))
+    roffs = torch.empty(sum(rc), dtype=torch.int64, device=flat.device)
+    if world > 1:
+        dist.all_to_all_single(rvals, vals, rc, sc, group=group)
+        dist.all_to_all_single(roffs, offs, rc, sc, group=group)
+    else:
+        rvals.copy_(vals)
+        roffs.copy_(offs)
+    mine = min(n, (rank + 1) * lp) - min(n, rank * lp)
+    if sum(rc) != mine:
+        raise ShapeMismatch(f"rank {rank} received {sum(rc)} elements for {mine} positions (layout not bijective?)")
+    out = flat.new_empty(mine)
+    out[roffs] = rvals
+    return out
 
 
 def transpose_rows_fused(local_rows, n_rows: int, n_cols: int, *, group=None):

@@ -233,3 +233,13 @@ def test_nw_more_strips_than_sms_and_large_index():
     sim = rng.integers(-10, 11, size=(n, n), dtype=np.int32)
     got = K.nw_score(torch.from_numpy(sim).cuda(), 10).cpu().numpy()
     np.testing.assert_array_equal(got, O.nw(sim, 10))
+
+
+def test_remap_sharded_single_rank_uses_the_gpu_map():
+    """shard.remap_sharded on one rank (no process group): the GPU map of the
+    local range, bucketing and placement reproduce kernels.remap."""
+    import paper_2505_08091_b200 as L
+    from paper_2505_08091_b200 import shard
+    g = L.parse_layout("GroupBy([2048,2048]).OrderBy(GenP([2048,2048], antidiag))")
+    x = torch.arange(2048 * 2048, device="cuda", dtype=torch.int32)
+    assert torch.equal(shard.remap_sharded(x, g), K.remap(x, None, g))

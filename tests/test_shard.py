@@ -166,3 +166,36 @@ def test_nw_bands_cover_the_strips_in_order():
         assert len(bands) == world and bands[0][0] == 0 and bands[-1][1] == nc
         assert all(b0[1] == b1[0] for b0, b1 in zip(bands, bands[1:]))
         assert all(e >= b for b, e in bands)
+
+
+
+def cpu_map(layout, first, count):
+    """layout.apply over logical indices first .. first+count-1 (scalar API)."""
+    dims = layout.dims
+    out = []
+    for v in range(first, first + count):
+        idx, rem = [], v
+        for d in reversed(dims):
+            idx.append(rem % d)
+            rem //= d
+        out.append(layout.apply(tuple(reversed(idx))))
+    return torch.tensor(out, dtype=torch.int64)
+
+
+def _remap_sharded_case(rank, world):
+    for dsl in ("GroupBy([8,8]).OrderBy(GenP([8,8], antidiag))",
+                "GroupBy([6,10]).OrderBy(RegP([2,3,2,5],[3,1,4,2]))",
+                "GroupBy([7,9]).OrderBy(Col(9,7))"):
+        g = L.parse_layout(dsl)
+        n = int(np.prod(g.dims))
+        full = (torch.arange(n, dtype=torch.int32) * 7 + 3)
+        lp = -(-n // world)
+        local = full[min(n, rank * lp):min(n, (rank + 1) * lp)]
+        got = shard.remap_sharded(local, g, compute_map=cpu_map)
+        whole = cpu_remap(full, None, g)
+        assert torch.equal(got, whole[min(n, rank * lp):min(n, (rank + 1) * lp)]), dsl
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_remap_sharded_any_bijective_layout(world):
+    run_world(_remap_sharded_case, world=world)
