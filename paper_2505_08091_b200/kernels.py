@@ -30,7 +30,7 @@ import threading
 from typing import Dict, Optional, Tuple
 
 from . import codegen, lower, runtime, staging
-from .errors import BijectivityViolation, ShapeMismatch, UnsupportedNode
+from .errors import BijectivityViolation, LegoError, ShapeMismatch, UnsupportedNode
 from .expr import IntConst, Var, VarRange
 from .simplify import _lin_of
 
@@ -126,6 +126,7 @@ def _program(key, builder, device: int):
 
 
 def index_map_source(layout) -> Tuple[str, runtime.ProgramInfo]:
+    check_genp_agreement(layout)
     x, app = lower.apply_map_expr(layout)
     injective = getattr(lower._group(layout), "injective", False)
     defines = {"LEGO_KIND": 0}
@@ -190,6 +191,8 @@ def plan_remap(src_layout, dst_layout, elem_bytes: int, route: Optional[Route] =
     position anyway and ignore it."""
     if elem_bytes not in (1, 2, 4, 8, 16):
         raise UnsupportedNode(f"element size {elem_bytes} not supported (1, 2, 4, 8 or 16 bytes)")
+    check_genp_agreement(src_layout)
+    check_genp_agreement(dst_layout)
     if route is not None:
         return _routed_plan(src_layout, dst_layout, elem_bytes, route)
     band = _band_plan(src_layout, dst_layout, elem_bytes)
@@ -616,6 +619,58 @@ def _untrusted_genps(layout) -> bool:
     g = lower._group(layout)
     return any(isinstance(p, GenP) and p.size > TRUST_BOUND and not _builtin_genp(p)
                for stage in g.orders for p in stage.perms)
+
+
+GENP_SAMPLES = 512          # points per user GenP checked before its first program
+
+
+def check_genp_agreement(layout, samples: int = GENP_SAMPLES) -> None:
+    """Every user GenP above the reference's trust bound must have a symbolic
+    builder that agrees with its concrete callable: the device runs the
+    symbolic form, the reference semantics is the concrete one
+    (layout.py:187-200), and validate() only compares them up to 4096 points
+    (layout.py:718-719).  Check ``samples`` deterministic points of each such
+    GenP (forward and, when present, inverse) and raise ``LegoError`` on a
+    disagreement, before any program is built from the layout."""
+    from .expr import IntConst, eval_expr
+    from .layout import GenP
+    if layout is None:
+        return
+    g = lower._group(layout)
+    for stage in g.orders:
+        for p in stage.perms:
+            if not (isinstance(p, GenP) and p.size > TRUST_BOUND and not _builtin_genp(p)):
+                continue
+            if _AGREED.get(id(p)) is p:
+                continue
+            n = p.size
+            step = max(1, n // samples) | 1
+            for k in range(min(samples, n)):
+                f = (k * step + (k * 7919) % step) % n
+                idx, rem = [], f
+                for d in reversed(p.shape):
+                    idx.append(rem % d)
+                    rem //= d
+                idx = tuple(reversed(idx))
+                want = p.fwd.concrete(idx)
+                got = eval_expr(as_expr_value(p.fwd.symbolic(tuple(IntConst(c) for c in idx))), {})
+                if got != want:
+                    raise LegoError(f"{p!r}: symbolic builder gives {got} at {idx}, the concrete function {want}; "
+                                    "the device would evaluate the symbolic form")
+                if p.inv_fn is not None:
+                    wi = tuple(p.inv_fn.concrete(want))
+                    gi = tuple(eval_expr(as_expr_value(e), {}) for e in p.inv_fn.symbolic(IntConst(want)))
+                    if gi != wi:
+                        raise LegoError(f"{p!r}: symbolic inverse gives {gi} at {want}, the concrete inverse {wi}")
+            _AGREED[id(p)] = p                  # keeps p alive, so its id is not reused
+
+
+_AGREED: dict = {}
+
+
+def as_expr_value(e):
+    from .expr import IntConst
+    return e if not isinstance(e, int) else IntConst(e)
 
 
 def _needs_bijectivity_gate(src_layout, dst_layout, plan):

@@ -120,3 +120,32 @@ def test_device_maps_and_remaps(name):
             got = K.remap(xd, lay, None).cpu().numpy()               # gather: out[x] = src[apply(x)]
             assert np.array_equal(got, x[app]), (name, dt, "gather")
             assert np.array_equal(x[app][inv], x)
+
+
+def test_disagreeing_symbolic_builder_is_rejected_before_any_program():
+    """A user GenP above the reference's 4096-point trust bound whose symbolic
+    builder (what the device runs) disagrees with its concrete callable (the
+    reference semantics) is refused when a program is planned from it."""
+    import paper_2505_08091_b200 as L
+    from paper_2505_08091_b200 import GenP, PermFn, kernels as K
+
+    def fwd(idx):
+        i, j = idx
+        return i * 128 + (j ^ 1)             # concrete: swap neighbouring columns
+
+    def fwd_sym(idx):
+        i, j = idx
+        return i * 128 + j                   # symbolic: identity (wrong)
+
+    def inv(f):
+        return f // 128, (f % 128) ^ 1
+
+    def inv_sym(f):
+        return f // 128, f % 128
+
+    bad = GenP((128, 128), PermFn(fwd, fwd_sym), PermFn(inv, inv_sym), name=None)
+    g = L.GroupBy([128, 128]).order_by(bad)
+    with pytest.raises(L.LegoError, match="symbolic"):
+        K.plan_remap(None, g, 4)
+    with pytest.raises(L.LegoError, match="symbolic"):
+        K.index_map_source(g)
