@@ -198,7 +198,8 @@ def gather_nw_bands(out, bands, *, group=None):
     b0, e0 = bands[rank]
     c0, c1 = 1 + 128 * b0, min(n, 128 * e0) + 1
     mine = out.new_zeros(*lead, n + 1, w)
-    mine[..., :, :c1 - c0] = out[..., :, c0:c1]
+    if c1 > c0:                                 # ranks past the last strip hold no columns
+        mine[..., :, :c1 - c0] = out[..., :, c0:c1]
     parts = [torch.empty_like(mine) for _ in bands]
     dist.all_gather(parts, mine.contiguous(), group=group)
     full = out.clone()

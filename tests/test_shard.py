@@ -199,3 +199,21 @@ def _remap_sharded_case(rank, world):
 @pytest.mark.parametrize("world", [2, 3])
 def test_remap_sharded_any_bijective_layout(world):
     run_world(_remap_sharded_case, world=world)
+
+
+def _gather_bands_case(rank, world):
+    n = 300                                     # 3 strips over 4 ranks: the last band is empty
+    bands = shard.nw_bands(n, world)
+    whole = torch.arange((n + 1) * (n + 1), dtype=torch.int32).reshape(n + 1, n + 1)
+    b0, e0 = bands[rank]
+    out = torch.full_like(whole, -1)
+    out[0, :] = whole[0, :]
+    out[:, 0] = whole[:, 0]
+    lo, hi = 1 + 128 * b0, min(n, 128 * e0) + 1
+    if hi > lo:
+        out[:, lo:hi] = whole[:, lo:hi]
+    assert torch.equal(shard.gather_nw_bands(out, bands), whole)
+
+
+def test_gather_nw_bands_with_an_empty_band():
+    run_world(_gather_bands_case, world=4)
