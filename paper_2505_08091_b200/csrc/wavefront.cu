@@ -64,8 +64,9 @@ static lego_status nw_scratch(cudaStream_t st, size_t words_bytes, int** ticket,
 
 int lego_nw_smem_bytes() { return nwk::SMEM_BYTES; }
 
-lego_status lego_nw_prepare(const int32_t* sim, int32_t* score, int64_t n, int32_t penalty, int64_t batch,
-                            int64_t tile_rows, int tiled, cudaStream_t st, NwPlan* plan) {
+// argument rules shared by every NW entry point; fills the border grid
+static lego_status nw_validate(const int32_t* sim, int32_t* score, int64_t n, int32_t penalty, int64_t batch,
+                               NwPlan* plan) {
     memset(plan, 0, sizeof *plan);
     if (n < 0 || batch < 0) return lego_fail(LEGO_E_SHAPE, "negative NW size");
     if (n > (1 << 20)) return lego_fail(LEGO_E_SHAPE, "NW n above 2^20");
@@ -79,7 +80,13 @@ lego_status lego_nw_prepare(const int32_t* sim, int32_t* score, int64_t n, int32
     plan->batch = batch;
     const long long bgrid = (batch * (n + 1) + 255) / 256;
     plan->border_ctas = (unsigned)(bgrid < 4096 ? bgrid : 4096);
-    if (n == 0) return LEGO_OK;
+    return LEGO_OK;
+}
+
+lego_status lego_nw_prepare(const int32_t* sim, int32_t* score, int64_t n, int32_t penalty, int64_t batch,
+                            int64_t tile_rows, int tiled, cudaStream_t st, NwPlan* plan) {
+    LEGO_TRY(nw_validate(sim, score, n, penalty, batch, plan));
+    if (batch == 0 || n == 0) return LEGO_OK;
     const long long H = tile_rows > 0 ? tile_rows : n;
     const long long nr = (n + H - 1) / H;
     const long long nc = (n + nwk::STRIP - 1) / nwk::STRIP;
@@ -155,7 +162,7 @@ extern "C" lego_status lego_nw_band_i32(const int32_t* sim, int32_t* score, int6
     const long long n_pad = (n + nwk::BLK - 1) / nwk::BLK * nwk::BLK;
     if (left_words && left_batch_stride < n_pad) return lego_fail(LEGO_E_ARG, "left_batch_stride below n_pad");
     NwPlan pl;
-    LEGO_TRY(lego_nw_prepare(sim, score, n, penalty, batch, n, 0, st, &pl));   // validation, borders grid
+    LEGO_TRY(nw_validate(sim, score, n, penalty, batch, &pl));   // the edge words are the caller's
     if (batch == 0) return LEGO_OK;
     int* ticket = nullptr;
     int* unused = nullptr;
