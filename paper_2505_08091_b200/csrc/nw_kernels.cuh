@@ -231,6 +231,12 @@ __device__ __forceinline__ int slot(int r, int g, int h) {
 #ifndef NW_ORDERED
 #define NW_ORDERED 1             // shuffle, S' store and prefetch of each slot issued in order (volatile asm)
 #endif
+#ifndef NW_SHFL3
+// lane 0's boundary as a third max operand (no select on the shuffle chain):
+// strips 882.9 -> 864.5 us; tiled programs measured slower with it (128-row
+// tiles 1584 -> 1623 us, 4096-row 1212 -> 1307), so strips only
+#define NW_SHFL3 (!NW_TILED)
+#endif
 #ifndef NW_QFORM
 #define NW_QFORM 1               // left-independent prefix maxima first: one max from the left value to x3
 #endif
@@ -388,11 +394,24 @@ __device__ __forceinline__ void nw_step(Lane& c, int s, int lane, unsigned char*
         const int q1 = max(max(cur[q].y + up0 + p2, up1), q0);
         const int q2 = max(max(cur[q].z + up1 + p2, up2), q1);
         const int q3 = max(max(cur[q].w + up2 + p2, up3), q2);
-        const int x3 = max_opaque(q3, left);
-#if NW_ORDERED
-        asm volatile("shfl.sync.up.b32 %0, %1, 1, 0, 0xffffffff;" : "=r"(c.lin[q]) : "r"(x3));
+#if NW_SHFL3
+        // lane 0's left value enters through a third operand fixed before the
+        // shuffle result arrives, so the shuffle chain has no select: lane 0's
+        // own shuffle returns its previous row's x3 = up3 <= q3 (a column of S'
+        // never decreases), which cannot change max(q3, boundary)
+        const int sh = c.lin[(q + RPS - SKEW) % RPS];
+        const int bvm = lane == 0 ? lb[q] : (-2147483647 - 1);
+        int x3;
+        asm("max.s32 %0, %1, %2;\n\tmax.s32 %0, %0, %3;" : "=&r"(x3) : "r"(q3), "r"(bvm), "r"(sh));
+        const int x3s = GUARD && !live ? up3 : x3;   // a dead slot shuffles a value its right lane may take as up3
 #else
-        c.lin[q] = __shfl_up_sync(0xffffffffu, x3, 1);
+        const int x3 = max_opaque(q3, left);
+        const int x3s = x3;
+#endif
+#if NW_ORDERED
+        asm volatile("shfl.sync.up.b32 %0, %1, 1, 0, 0xffffffff;" : "=r"(c.lin[q]) : "r"(x3s));
+#else
+        c.lin[q] = __shfl_up_sync(0xffffffffu, x3s, 1);
 #endif
         const int x0 = max_opaque(q0, left);
         const int x1 = max_opaque(q1, left);
